@@ -1,0 +1,336 @@
+"""Benchmark of the B200 j2d5pt deep-temporal-blocking solve.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload c2|c1|c3a|c3b|c4|c5]
+
+A bench "step" is one complete solve of the workload (e.g. C2 = all 10,000
+Jacobi steps of a 1900^2 fp64 grid), inputs already resident in HBM
+(generated on the device by the splitmix64 fill kernel, bit-identical to the
+reference's random_interior). Metric (BASELINE.json): GCells/s = valid
+cell-updates nx*ny*steps per second. Prints ONE JSON line on rank 0.
+
+--impl reference times the reference's CPU algorithm (the pinned numpy
+restatement of jacobi_reference in oracle/, single-threaded by contract) on
+a bounded sample of the same workload on this host.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (nx, ny, steps, dtype, description)
+    "c1": (256, 256, 100, "f64", "j2d5pt fp64 256x256, 100 steps (BASELINE config 1)"),
+    "c2": (1900, 1900, 10000, "f64", "j2d5pt fp64 1900x1900, 10000 steps, smem-resident (BASELINE config 2)"),
+    "c3a": (2700, 2700, 10000, "f32", "j2d5pt fp32 2700x2700, 10000 steps, smem-resident (BASELINE config 3)"),
+    "c3b": (8192, 8192, 1000, "f32", "j2d5pt fp32 8192x8192, 1000 steps, streaming (BASELINE config 3)"),
+    "c4": (16384, 16384, 1000, "f64", "j2d5pt fp64 16384x16384, 1000 steps, streaming (BASELINE config 4)"),
+}
+
+METRIC = "j2d5pt GCells/s (fp64/fp32) at 1/2/4/8 B200 vs roofline and CPU reference"
+
+
+def measured_peaks():
+    """Roofline denominators: HBM from MEASURED_PEAKS.json (driver-written);
+    smem and FP64/FP32 issue rates from this repo's B200 microbenchmarks
+    (tools/microbench/peaks.cu, profiles/r01_microbench_peaks.log)."""
+    peaks = {"hbm_gbs": 6545.3, "hbm_src": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            mp = json.load(fh)
+        peaks["hbm_gbs"] = float(mp["hbm_gbs"])
+        peaks["hbm_src"] = "MEASURED_PEAKS.json"
+    except (OSError, KeyError, ValueError):
+        pass
+    # microbench (148 SMs): LDS.128 235.2 B/SM/ns; DMUL/DADD 124.6 /SM/ns; FMUL/FADD 244.9 /SM/ns
+    peaks["smem_gbs"] = 235.156 * 148
+    peaks["fp64_gops"] = 124.563 * 148
+    peaks["fp32_gops"] = 244.929 * 148
+    return peaks
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference_sample(nx, ny, dtype, budget_s=10.0):
+    """Time the reference algorithm (numpy restatement of jacobi_reference,
+    oracle.py:19-34, pinned bitwise to the reference) on this host's cores."""
+    import numpy as np
+    from oracle import jacobi_numpy
+    from paper_2306_03336_b200.grid import grid_new
+    from paper_2306_03336_b200.prng import random_interior
+    dt = np.float64 if dtype == "f64" else np.float32
+    g = grid_new(nx, ny, random_interior(nx, ny, 1))
+    w = (0.2, 0.2, 0.2, 1.0 - 4 * 0.2, 0.2)
+    t0 = time.perf_counter()
+    jacobi_numpy(g.data, w, 2, dt)
+    probe = max(time.perf_counter() - t0, 1e-6) / 2
+    steps = max(1, min(2000, int(budget_s / probe)))
+    t0 = time.perf_counter()
+    jacobi_numpy(g.data, w, steps, dt)
+    el = time.perf_counter() - t0
+    return {"value": nx * ny * steps / el / 1e9, "unit": "GCells/s", "cores": 1, "kind": "port",
+            "sample": f"{nx}x{ny} {dtype}, {steps} steps of the numpy restatement of "
+                      f"jacobi_reference (oracle/ref.py, pinned to the reference), 1 core, "
+                      f"{el:.1f} s"}
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup(args)
+    if rank != 0:
+        return
+    nx, ny, steps, dtype, desc = WORKLOADS[args.workload]
+    import numpy as np
+    from oracle import jacobi_numpy
+    from paper_2306_03336_b200.grid import grid_new
+    from paper_2306_03336_b200.prng import random_interior
+    dt = np.float64 if dtype == "f64" else np.float32
+    g = grid_new(nx, ny, random_interior(nx, ny, 1))
+    w = (0.2, 0.2, 0.2, 1.0 - 4 * 0.2, 0.2)
+    # bounded sample per bench step: ~1 s of the reference's own per-step cost
+    t0 = time.perf_counter()
+    jacobi_numpy(g.data, w, 1, dt)
+    one = max(time.perf_counter() - t0, 1e-6)
+    sample = max(1, min(steps, int(1.0 / one)))
+    for _ in range(args.warmup):
+        jacobi_numpy(g.data, w, sample, dt)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        jacobi_numpy(g.data, w, sample, dt)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = nx * ny * sample * args.steps / total / 1e9
+    line = {"metric": METRIC, "value": value, "unit": "GCells/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+            "config": {"workload": desc, "nx": nx, "ny": ny, "solve_steps": steps,
+                       "sample_steps_per_bench_step": sample},
+            "cpu_baseline": {"value": value, "unit": "GCells/s", "cores": 1, "kind": "port",
+                             "sample": f"{nx}x{ny} {dtype}, {sample} Jacobi steps per bench step "
+                                       "(numpy restatement of jacobi_reference, 1 core: the "
+                                       "reference oracle is single-threaded by contract)"},
+            "e2e": {"value": value, "unit": "GCells/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    import numpy as np
+    import torch
+    world, rank, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    from paper_2306_03336_b200 import StencilWeights, j2d5pt_device, last_launch_count, plan_b200
+    from paper_2306_03336_b200 import _native
+    from paper_2306_03336_b200.prng import fill_random_device
+
+    nx, ny, steps, dtype, desc = WORKLOADS[args.workload]
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    elem = 8 if dtype == "f64" else 4
+    w = StencilWeights.diffusive(0.2)
+    dev = torch.device("cuda", local)
+    a = torch.empty((ny + 2, nx + 2), dtype=tdt, device=dev)
+    b = torch.empty_like(a)
+    fill_random_device(a, nx, ny, 1, ghost=0.0)
+    plan = plan_b200(nx, ny, elem, steps, 1)
+    grid_bytes = a.numel() * elem
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # 256 MB > L2
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        j2d5pt_device(a, b, nx, ny, w, steps)
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    launches = 0
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i)  # evict the grid from L2 between timed iterations
+            torch.cuda.synchronize()
+            barrier()
+            ev[i][0].record(stream)
+            j2d5pt_device(a, b, nx, ny, w, steps)
+            ev[i][1].record(stream)
+            launches += last_launch_count()
+            torch.cuda.synchronize()
+            barrier()
+    ms = [s.elapsed_time(e) for s, e in ev]
+    total_ms = sum(ms)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    cells = nx * ny * steps
+    value = world * cells * args.steps / (total_ms * 1e-3) / 1e9
+
+    # e2e through the public host API (H2D + solve + D2H from pinned host memory)
+    e2e = None
+    if rank == 0:
+        host_in = torch.empty((ny + 2, nx + 2), dtype=tdt, pin_memory=True)
+        host_in.copy_(a.cpu())
+        host_out = torch.empty_like(host_in).pin_memory()
+        import ctypes
+        lib = _native.lib()
+        fn = lib.dtb_j2d5pt_f64 if dtype == "f64" else lib.dtb_j2d5pt_f32
+        ct = ctypes.c_double if dtype == "f64" else ctypes.c_float
+        wts = (ct * 5)(*w.astuple())
+        rep = _native.DtbReport()
+        call = lambda: fn(host_in.data_ptr(), host_out.data_ptr(), nx, ny, nx + 2, wts, steps,
+                          1, None, 1, 1, 0, ctypes.byref(rep))
+        if call() != 0:
+            raise RuntimeError(_native.last_error())
+        k = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(k):
+            if call() != 0:
+                raise RuntimeError(_native.last_error())
+        el = time.perf_counter() - t0
+        e2e = {"value": cells * k / el / 1e9, "unit": "GCells/s",
+               "h2d_bytes_per_step": grid_bytes, "d2h_bytes_per_step": grid_bytes,
+               "api": "dtb_j2d5pt_%s (include/dtb_b200.h) from pinned host buffers" % dtype}
+        res = host_out.numpy()
+        if not np.isfinite(res).all():
+            raise RuntimeError("non-finite result")
+
+    if rank != 0:
+        return
+    peaks = measured_peaks()
+    kernel_s = total_ms * 1e-3 / args.steps
+    cells_per_s = cells / kernel_s
+    fp_peak = peaks["fp64_gops"] if elem == 8 else peaks["fp32_gops"]
+    rooflines = {
+        "smem": {"achieved": cells_per_s * 2 * elem / 1e9, "peak": peaks["smem_gbs"], "unit": "GB/s",
+                 "bytes_per_cell": 2 * elem, "peak_src": "microbench LDS.128 (profiles/r01_microbench_peaks.log)"},
+        "fp_pipe": {"achieved": cells_per_s * 9 / 1e9, "peak": fp_peak, "unit": "Gop/s",
+                    "ops_per_cell": 9, "peak_src": "microbench DMUL/DADD (profiles/r01_microbench_peaks.log)"},
+        "hbm": {"achieved": cells_per_s * 2 * elem / max(plan.halo, 1) / 1e9
+                if plan.mode == "streaming" else grid_bytes * 2 / kernel_s / 1e9,
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "peak_src": peaks["hbm_src"]},
+    }
+    for r in rooflines.values():
+        r["frac"] = r["achieved"] / r["peak"]
+    if plan.mode == "resident":
+        main = dict(rooflines["smem"], bound="smem")
+    else:
+        main = dict(rooflines["hbm"], bound="hbm")
+    main["traffic"] = None
+    main["kernel"] = "resident_kernel" if plan.mode == "resident" else "stream_kernel"
+    line = {
+        "metric": METRIC, "value": value, "unit": "GCells/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+        "data": "synthetic (splitmix64 random_interior seed 1, generated on device)",
+        "config": {"workload": desc, "nx": nx, "ny": ny, "solve_steps": steps,
+                   "weights": "diffusive(0.2)", "l2": "256 MB buffer written between timed iterations",
+                   "plan": {"mode": plan.mode, "halo": plan.halo, "lane_elems": plan.lane_elems,
+                            "warps": plan.warps, "tiles": [plan.tiles_x, plan.tiles_y],
+                            "ctas": plan.ctas, "smem_bytes": plan.smem_bytes}},
+        "roofline": main,
+        "rooflines": rooflines,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "cpu_baseline": cpu_reference_sample(min(nx, 1900), min(ny, 1900), dtype)
+        if not args.no_cpu else None,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)  # the timing rules require >= 3 warm-up steps
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,136 @@
+/*
+ * dtb_b200.h — C ABI of the B200-native deep-temporal-blocking j2d5pt solver.
+ *
+ * This is the drop-in boundary for the reference's hot path. The reference
+ * (arxiv 2306.03336 package `dtb`) is pure Python and has no FFI layer; its
+ * boundary is the Python API, which the ctypes host mirror
+ * paper_2306_03336_b200/engine.py re-exposes on top of these entry points:
+ *
+ *   dtb_j2d5pt_f64  replaces  dtb.engine.run_dtb        (pkg/src/dtb/engine.py:305-326)
+ *                   and       dtb.oracle.jacobi_reference (pkg/src/dtb/oracle.py:19-34)
+ *                   (same padded float64 (ny+2) x (nx+2) C-order buffer, grid.py:126-162;
+ *                   same W,E,S,C,N weight order, grid.py:95-123; same valid-region
+ *                   freezing, engine.py:26-30; same TrafficReport fields, metrics.py:39-66)
+ *   dtb_j2d5pt_f32  fp32 twin (the reference has no fp32 path; BASELINE configs C3a/C3b)
+ *   dtb_plan        replaces  dtb.planner.plan_device_tiles (planner.py:188-243) for the
+ *                   B200 execution (single-buffer in-place smem model)
+ *   dtb_last_error  the message the reference would put in its exception
+ *
+ * Buffers are caller-owned, row-major, (ny+2) rows of `pitch` elements
+ * (pitch >= nx+2); `out` is fully written, ghost ring included (copied from
+ * `in`). `in` is never modified. Calls are blocking and externally
+ * synchronous (SPEC: one caller at a time per process).
+ *
+ * Results are bitwise identical to the reference's jacobi_reference: every
+ * cell update is ((((W*w + E*e) + S*s) + C*c) + N*n) with every product and
+ * sum rounded separately (no FMA).
+ */
+#ifndef DTB_B200_H
+#define DTB_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the Python mirror maps them onto the reference's exceptions */
+#define DTB_OK 0
+#define DTB_EINVAL 1       /* ValueError      (engine.py:236-248, grid.py:111-115) */
+#define DTB_ERANGE 2       /* IndexError      (engine.py:249-251, kernel.py:85-91) */
+#define DTB_EINFEASIBLE 3  /* InfeasiblePlanError (planner.py:51-56, 222-228) */
+#define DTB_ECUDA 4        /* EngineError: CUDA runtime failure (engine.py:49-50) */
+#define DTB_ECAPACITY 5    /* EngineError: capacity contract (engine.py:141-145) */
+
+/* flags */
+#define DTB_FLAG_POISON 1u          /* NaN-fill scratch that no valid cell may read (engine.py:16-20,174-177) */
+#define DTB_FLAG_FORCE_STREAM 2u    /* use the streaming (T-fused HBM pass) kernel even if resident fits */
+#define DTB_FLAG_FORCE_NAIVE 4u     /* one global-memory step per launch (the T=1 HBM baseline) */
+#define DTB_FLAG_FORCE_DEPTH 8u     /* use t_depth as the temporal halo depth instead of the planner's */
+
+/* Half-open rectangle in interior coordinates (grid.py:38-92). */
+typedef struct dtb_rect {
+  int64_t x0, y0, width, height;
+} dtb_rect;
+
+/* Cell-granular traffic of the B200 execution (metrics.py:39-66 field order). */
+typedef struct dtb_report {
+  int64_t global_load_cells;
+  int64_t global_store_cells;
+  int64_t halo_exchanged_cells;
+  int64_t redundant_compute_cells;
+  int64_t useful_compute_cells;
+  int64_t scratchpad_peak_bytes;
+  int64_t elem_bytes;
+} dtb_report;
+
+/* The B200 plan (what plan_device_tiles' TilingPlan is for the reference). */
+typedef struct dtb_plan_info {
+  int32_t mode;         /* 0 resident (persistent, smem-resident), 1 streaming, 2 naive */
+  int32_t elem_bytes;
+  int32_t lane_elems;   /* K: consecutive columns per lane */
+  int32_t warps;        /* warps per CTA (row bands) */
+  int32_t halo;         /* temporal halo depth h = steps per exchange / per HBM pass */
+  int32_t tiles_x, tiles_y;
+  int32_t ctas;         /* grid size of the launch */
+  int32_t ctas_per_sm;
+  int32_t dyn;          /* 1 if a tile's right frozen column is not lane-aligned */
+  int64_t smem_bytes;   /* dynamic shared memory per CTA */
+  int64_t tile_w, tile_h;                 /* largest owned tile */
+  int64_t load_w, load_h;                 /* largest load region */
+  int64_t computed_cells_per_step;        /* lane-cells updated per step, all tiles */
+  double est_cells_per_clk;               /* planner cost model */
+} dtb_plan_info;
+
+/* Host-buffer entry points (H2D + solve + D2H). n_gpus >= 1; t_depth >= 1 is
+ * the reference plan's depth: total_steps must be a positive multiple of it
+ * (engine.py:238-240). valid may be NULL (whole interior). ilp is accepted for
+ * API parity (KernelConfig, kernel.py:33-41) and must be >= 1; it cannot
+ * change results. rep may be NULL. */
+int dtb_j2d5pt_f64(const double* in, double* out, int64_t nx, int64_t ny, int64_t pitch,
+                   const double w[5], int64_t total_steps, int64_t t_depth,
+                   const dtb_rect* valid, int ilp, int n_gpus, unsigned flags,
+                   dtb_report* rep);
+int dtb_j2d5pt_f32(const float* in, float* out, int64_t nx, int64_t ny, int64_t pitch,
+                   const float w[5], int64_t total_steps, int64_t t_depth,
+                   const dtb_rect* valid, int ilp, int n_gpus, unsigned flags,
+                   dtb_report* rep);
+
+/* Device-pointer entry points on the current device; `stream` is a
+ * cudaStream_t (NULL = legacy default). Asynchronous with respect to the host
+ * except for plan/scratch setup; in and out must not alias. */
+int dtb_j2d5pt_f64_dev(const double* d_in, double* d_out, int64_t nx, int64_t ny,
+                       int64_t pitch, const double w[5], int64_t total_steps,
+                       int64_t t_depth, const dtb_rect* valid, unsigned flags,
+                       void* stream, dtb_report* rep);
+int dtb_j2d5pt_f32_dev(const float* d_in, float* d_out, int64_t nx, int64_t ny,
+                       int64_t pitch, const float w[5], int64_t total_steps,
+                       int64_t t_depth, const dtb_rect* valid, unsigned flags,
+                       void* stream, dtb_report* rep);
+
+/* Plan without executing (the B200 analogue of plan_device_tiles). */
+int dtb_plan(int64_t nx, int64_t ny, int32_t elem_bytes, int64_t total_steps,
+             int64_t t_depth, unsigned flags, dtb_plan_info* out);
+
+/* Kernel launches issued by the most recent solve on this thread. */
+int64_t dtb_last_launch_count(void);
+
+/* Device properties the planner uses (cudaDeviceGetAttribute). */
+int dtb_device_info(int32_t* sms, int64_t* smem_optin_per_block, int64_t* l2_bytes,
+                    int32_t* cc_major, int32_t* cc_minor);
+
+/* On-device splitmix64 fill, bit-identical to grid_new(nx, ny,
+ * random_interior(nx, ny, seed), ghost) (prng.py:45-67, grid.py:165-196). */
+int dtb_fill_random_f64(double* d_out, int64_t nx, int64_t ny, int64_t pitch,
+                        uint64_t seed, double ghost, void* stream);
+int dtb_fill_random_f32(float* d_out, int64_t nx, int64_t ny, int64_t pitch,
+                        uint64_t seed, double ghost, void* stream);
+
+/* Last error message on this thread ("" if none). */
+const char* dtb_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DTB_B200_H */

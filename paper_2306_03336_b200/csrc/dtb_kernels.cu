@@ -1,0 +1,733 @@
+// dtb_kernels.cu — sm_100a kernels and the C ABI (include/dtb_b200.h).
+//
+//   resident_kernel  persistent cooperative launch, one CTA per SM; the whole
+//                    grid stays in shared memory for the whole solve. Every h
+//                    steps each CTA publishes the owned cells its neighbours'
+//                    halos cover into an L2-resident exchange buffer, bumps an
+//                    epoch flag (release), waits only for its <= 8 neighbours'
+//                    flags (acquire) and refreshes its halo ring. Replaces the
+//                    reference's serial-tile BSP loop (engine.py:265-290) and
+//                    its modelled "grid-level barrier".
+//   stream_kernel    one HBM pass: every tile loads owned+h halo from `src`,
+//                    fuses h steps in smem, stores owned cells to `dst`.
+//   naive_kernel     one global-memory step per launch (T=1 baseline).
+//   fill_random      on-device splitmix64, bit-identical to prng.py:45-67.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/dtb_b200.h"
+#include "dtb_core.cuh"
+#include "dtb_plan.h"
+
+namespace dtb {
+
+constexpr int kMaxTiles = 512;  // per dimension
+
+// 32 B of state per lane-row -> 16 warps (<=128 regs); 64 B -> 8 warps (<=255 regs)
+template <typename T, int K>
+struct Shape {
+  static constexpr int kThreads = (K * (int)sizeof(T) <= 32) ? 512 : 256;
+};
+
+// Tile geometry as kernel parameters (<= 32 KB param space on sm_70+ / CUDA 12.1+).
+// col[i] = (owned x0, owned x1, load x0, load x1) in interior coordinates.
+struct Geometry {
+  int ntx, nty;
+  int4 col[kMaxTiles];
+  int4 row[kMaxTiles];
+};
+
+template <typename T>
+struct Problem {
+  const T* in;
+  T* out;
+  int64_t pitch;  // elements per row of in/out
+  int nx, ny;
+  Weights<T> wt;
+};
+
+// ---------------------------------------------------------------------------
+// global <-> smem movement (coalesced along x: one warp per row, lanes stride)
+// ---------------------------------------------------------------------------
+template <typename T, int K>
+__device__ void load_region(T* tile, const T* __restrict__ g, int64_t pitch, int gx0, int gy0,
+                            int Lw, int Lh, int r0, int r1, int c0, int c1) {
+  // copy tile rows [r0,r1) x cols [c0,c1) from global padded coords (gy0+r, gx0+c)
+  typedef Tile<T, K> L;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  (void)Lw; (void)Lh;
+  for (int r = r0 + warp; r < r1; r += nw) {
+    const T* src = g + (int64_t)(gy0 + r) * pitch + gx0;
+    T* dst = tile + r * L::ROW;
+#pragma unroll 4
+    for (int c = c0 + lane; c < c1; c += 32) {
+      dst[L::swz(c / L::EPC) * L::EPC + (c % L::EPC)] = __ldcg(src + c);
+    }
+  }
+}
+
+template <typename T, int K>
+__device__ void store_region(const T* tile, T* __restrict__ g, int64_t pitch, int gx0, int gy0,
+                             int r0, int r1, int c0, int c1) {
+  typedef Tile<T, K> L;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int r = r0 + warp; r < r1; r += nw) {
+    T* dst = g + (int64_t)(gy0 + r) * pitch + gx0;
+    const T* src = tile + r * L::ROW;
+#pragma unroll 4
+    for (int c = c0 + lane; c < c1; c += 32) {
+      dst[c] = src[L::swz(c / L::EPC) * L::EPC + (c % L::EPC)];
+    }
+  }
+}
+
+// Poison (debug, DTB_FLAG_POISON): NaN every tile cell a correct schedule can
+// no longer read after `done` steps of the epoch — the ring of width `done`
+// along halo sides (the trapezoid rim, planner.py:272-286) plus the unused
+// lane columns. A stale read anywhere then propagates NaN into the owned
+// cells and fails the bitwise comparison (the reference's poison mode,
+// engine.py:16-20,174-177).
+template <typename T, int K>
+__device__ void poison_rim(T* tile, int Lw, int Lh, int done, bool hl, bool hr, bool ht, bool hb) {
+  typedef Tile<T, K> L;
+  const T nanv = (T)NAN;
+  for (int i = threadIdx.x; i < Lh * L::ROW; i += blockDim.x) {
+    const int r = i / L::ROW, c = i % L::ROW;
+    bool p = c >= Lw;
+    p |= hl && c < done;
+    p |= hr && c >= Lw - done;
+    p |= ht && r < done;
+    p |= hb && r >= Lh - done;
+    if (p) tile[L::at(r, c)] = nanv;
+  }
+}
+
+template <typename T, int K, bool DYN>
+__device__ void advance(T* tile, int Lw, int Lh, int steps, const Weights<T>& wt, bool poison,
+                        bool hl, bool hr, bool ht, bool hb) {
+  if (!poison) {
+    advance_tile<T, K, DYN>(tile, Lw, Lh, steps, wt);
+    return;
+  }
+  // poison mode: one step at a time, NaN the stale rim after each
+  for (int s = 0; s < steps; ++s) {
+    advance_tile<T, K, DYN>(tile, Lw, Lh, 1, wt);
+    poison_rim<T, K>(tile, Lw, Lh, s + 1, hl, hr, ht, hb);
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// streaming: one pass of h fused steps over every tile
+// ---------------------------------------------------------------------------
+template <typename T, int K, bool DYN>
+__global__ void __launch_bounds__(Shape<T, K>::kThreads, 1)
+stream_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int nx, int ny,
+              Weights<T> wt, int steps, int poison, const __grid_constant__ Geometry geo) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* tile = reinterpret_cast<T*>(smem_raw);
+  const int ntiles = geo.ntx * geo.nty;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int tx = t % geo.ntx, ty = t / geo.ntx;
+    const int4 cx = geo.col[tx], cy = geo.row[ty];
+    const int Lw = cx.w - cx.z, Lh = cy.w - cy.z;
+    // load region in padded coordinates = interior + 1
+    load_region<T, K>(tile, src, pitch, cx.z + 1, cy.z + 1, Lw, Lh, 0, Lh, 0, Lw);
+    __syncthreads();
+    advance<T, K, DYN>(tile, Lw, Lh, steps, wt, poison != 0, cx.z > -1, cx.w < nx + 1,
+                       cy.z > -1, cy.w < ny + 1);
+    // owned cells, plus the ghost ring where the tile touches the domain edge
+    const int sx0 = cx.x - (cx.x == 0), sx1 = cx.y + (cx.y == nx);
+    const int sy0 = cy.x - (cy.x == 0), sy1 = cy.y + (cy.y == ny);
+    store_region<T, K>(tile, dst, pitch, cx.z + 1, cy.z + 1, sy0 - cy.z, sy1 - cy.z, sx0 - cx.z,
+                       sx1 - cx.z);
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// resident: persistent cooperative kernel, neighbour-flag halo exchange
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename T, int K, bool DYN>
+__global__ void __launch_bounds__(Shape<T, K>::kThreads, 1)
+resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ xb0,
+                T* __restrict__ xb1, int* __restrict__ flags, int64_t pitch, int nx, int ny,
+                Weights<T> wt, int64_t total_steps, int h, int poison,
+                const __grid_constant__ Geometry geo) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* tile = reinterpret_cast<T*>(smem_raw);
+  const int tx = blockIdx.x % geo.ntx, ty = blockIdx.x / geo.ntx;
+  const int4 cx = geo.col[tx], cy = geo.row[ty];
+  const int Lw = cx.w - cx.z, Lh = cy.w - cy.z;
+  const int gx0 = cx.z + 1, gy0 = cy.z + 1;  // padded coords of tile (0,0)
+  const bool hl = cx.z > -1, hr = cx.w < nx + 1, ht = cy.z > -1, hb = cy.w < ny + 1;
+
+  load_region<T, K>(tile, in, pitch, gx0, gy0, Lw, Lh, 0, Lh, 0, Lw);
+  __syncthreads();
+
+  // how deep each neighbour's load region reaches into my owned cells
+  const int bl = tx > 0 ? max(0, geo.col[tx - 1].w - cx.x) : 0;
+  const int br = tx + 1 < geo.ntx ? max(0, cx.y - geo.col[tx + 1].z) : 0;
+  const int bt = ty > 0 ? max(0, geo.row[ty - 1].w - cy.x) : 0;
+  const int bb = ty + 1 < geo.nty ? max(0, cy.y - geo.row[ty + 1].z) : 0;
+  // owned rect in tile coordinates
+  const int ox0 = cx.x - cx.z, ox1 = cx.y - cx.z, oy0 = cy.x - cy.z, oy1 = cy.y - cy.z;
+  // halo ring cells to refresh exclude the frozen ghost ring of the domain
+  const int rx0 = hl ? 0 : 1, rx1 = hr ? Lw : Lw - 1, ry0 = ht ? 0 : 1, ry1 = hb ? Lh : Lh - 1;
+
+  int64_t done = 0;
+  int epoch = 0;
+  while (true) {
+    const int steps = (int)((total_steps - done) < (int64_t)h ? (total_steps - done) : (int64_t)h);
+    advance<T, K, DYN>(tile, Lw, Lh, steps, wt, poison != 0, hl, hr, ht, hb);
+    done += steps;
+    if (done >= total_steps) break;
+    ++epoch;
+    T* xb = (epoch & 1) ? xb1 : xb0;
+    // 1. publish the owned band the neighbours' halos cover
+    if (bt) store_region<T, K>(tile, xb, pitch, gx0, gy0, oy0, oy0 + bt, ox0, ox1);
+    if (bb) store_region<T, K>(tile, xb, pitch, gx0, gy0, oy1 - bb, oy1, ox0, ox1);
+    if (bl) store_region<T, K>(tile, xb, pitch, gx0, gy0, oy0, oy1, ox0, ox0 + bl);
+    if (br) store_region<T, K>(tile, xb, pitch, gx0, gy0, oy0, oy1, ox1 - br, ox1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      st_release(flags + blockIdx.x, epoch);
+    }
+    // 2. wait for the (up to 8) neighbours of this epoch
+    if (threadIdx.x < 9 && threadIdx.x != 4) {
+      const int dx = (int)threadIdx.x % 3 - 1, dy = (int)threadIdx.x / 3 - 1;
+      const int nxt = tx + dx, nyt = ty + dy;
+      if (nxt >= 0 && nxt < geo.ntx && nyt >= 0 && nyt < geo.nty) {
+        const int* f = flags + nyt * geo.ntx + nxt;
+        while (ld_acquire(f) < epoch) __nanosleep(32);
+      }
+    }
+    __syncthreads();
+    // 3. refresh the halo ring (load region minus owned, domain ghost excluded)
+    if (ry0 < oy0) load_region<T, K>(tile, xb, pitch, gx0, gy0, Lw, Lh, ry0, oy0, rx0, rx1);
+    if (oy1 < ry1) load_region<T, K>(tile, xb, pitch, gx0, gy0, Lw, Lh, oy1, ry1, rx0, rx1);
+    if (rx0 < ox0) load_region<T, K>(tile, xb, pitch, gx0, gy0, Lw, Lh, oy0, oy1, rx0, ox0);
+    if (ox1 < rx1) load_region<T, K>(tile, xb, pitch, gx0, gy0, Lw, Lh, oy0, oy1, ox1, rx1);
+    __syncthreads();
+  }
+  const int sx0 = ox0 - !hl, sx1 = ox1 + !hr, sy0 = oy0 - !ht, sy1 = oy1 + !hb;
+  store_region<T, K>(tile, out, pitch, gx0, gy0, sy0, sy1, sx0, sx1);
+}
+
+// ---------------------------------------------------------------------------
+// naive: one step, global memory (the T=1 HBM baseline)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void naive_kernel(const T* __restrict__ a, T* __restrict__ b, int64_t pitch, int nx,
+                             int ny, Weights<T> wt) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int y = blockIdx.y; y < ny + 2; y += gridDim.y) {
+    if (x >= nx + 2) return;
+    const int64_t i = (int64_t)y * pitch + x;
+    if (x == 0 || y == 0 || x == nx + 1 || y == ny + 1) {
+      b[i] = a[i];
+    } else {
+      b[i] = cell_update(a[i - 1], a[i + 1], a[i - pitch], a[i], a[i + pitch], wt);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// splitmix64 fill (prng.py:45-67): interior (x, y) = value i = y*nx + x
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void fill_random_kernel(T* out, int64_t pitch, int nx, int ny, uint64_t seed,
+                                   double ghost) {
+  const int64_t total = (int64_t)(nx + 2) * (ny + 2);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t y = k / (nx + 2), x = k % (nx + 2);
+    double v;
+    if (x == 0 || y == 0 || x == nx + 1 || y == ny + 1) {
+      v = ghost;
+    } else {
+      const uint64_t i = (uint64_t)((y - 1) * nx + (x - 1));
+      uint64_t z = seed + (i + 1) * 0x9E3779B97F4B7C15ull;
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      z = z ^ (z >> 31);
+      v = (double)(z >> 11) * (1.0 / 9007199254740992.0);
+    }
+    out[y * pitch + x] = (T)v;
+  }
+}
+
+}  // namespace dtb
+
+// ===========================================================================
+// host runtime + C ABI
+// ===========================================================================
+namespace {
+
+using namespace dtb;
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(DTB_ECUDA, "CUDA error %s (%s) at %s:%d", cudaGetErrorName(e_),        \
+                  cudaGetErrorString(e_), __FILE__, __LINE__);                           \
+  } while (0)
+
+// Per-device scratch, grown on demand and kept (the solve is externally
+// synchronous, so one arena per device suffices).
+struct Arena {
+  void* p = nullptr;
+  size_t n = 0;
+};
+std::mutex g_mu;
+Arena g_scratch[16];
+Arena g_io[16];
+
+int arena_get(Arena& a, size_t bytes, void** out) {
+  if (a.n < bytes) {
+    if (a.p) cudaFree(a.p);
+    a.p = nullptr;
+    a.n = 0;
+    CUDA_TRY(cudaMalloc(&a.p, bytes));
+    a.n = bytes;
+  }
+  *out = a.p;
+  return DTB_OK;
+}
+
+int query_dev(DevInfo& d) {
+  int dev = 0, v = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+  d.sms = v;
+  CUDA_TRY(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  d.smem_optin = v;
+  CUDA_TRY(cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev));
+  d.l2_bytes = v;
+  CUDA_TRY(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  d.smem_per_sm = v;
+  return DTB_OK;
+}
+
+int fill_geometry(const Plan& p, Geometry& g) {
+  if (p.sx.n > kMaxTiles || p.sy.n > kMaxTiles)
+    return fail(DTB_EINFEASIBLE, "plan needs %d x %d tiles (max %d per dimension)", p.sx.n,
+                p.sy.n, kMaxTiles);
+  memset(&g, 0, sizeof g);
+  g.ntx = p.sx.n;
+  g.nty = p.sy.n;
+  for (int i = 0; i < p.sx.n; ++i) g.col[i] = make_int4(p.sx.o0[i], p.sx.o1[i], p.sx.l0[i], p.sx.l1[i]);
+  for (int j = 0; j < p.sy.n; ++j) g.row[j] = make_int4(p.sy.o0[j], p.sy.o1[j], p.sy.l0[j], p.sy.l1[j]);
+  return DTB_OK;
+}
+
+template <typename T>
+Weights<T> to_weights(const T w[5]) {
+  Weights<T> k;
+  k.w = w[0]; k.e = w[1]; k.s = w[2]; k.c = w[3]; k.n = w[4];
+  return k;
+}
+
+template <typename T, int K, bool DYN>
+int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_out,
+                        int64_t pitch, int nx, int ny, const Weights<T>& wt,
+                        int64_t steps, bool poison, cudaStream_t st) {
+  const int threads = Shape<T, K>::kThreads;
+  if (threads != p.warps * 32)
+    return fail(DTB_EINFEASIBLE, "plan warps %d do not match kernel shape %d", p.warps, threads / 32);
+  const int smem = (int)p.smem_bytes;
+  const int dev = 0;
+  (void)dev;
+  const size_t grid_bytes = (size_t)(ny + 2) * pitch * sizeof(T);
+  int device;
+  CUDA_TRY(cudaGetDevice(&device));
+  if (p.mode == 0) {
+    auto kern = resident_kernel<T, K, DYN>;
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int per_sm = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+    int sms = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    if (per_sm < 1 || p.ctas > per_sm * sms)
+      return fail(DTB_ECAPACITY, "resident plan needs %d co-resident CTAs, device holds %d",
+                  p.ctas, per_sm * sms);
+    void* scratch = nullptr;
+    const size_t flag_bytes = 256 + (size_t)p.ctas * sizeof(int);
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      int rc = arena_get(g_scratch[device & 15], 2 * grid_bytes + flag_bytes, &scratch);
+      if (rc) return rc;
+    }
+    T* xb0 = reinterpret_cast<T*>(scratch);
+    T* xb1 = reinterpret_cast<T*>(reinterpret_cast<char*>(scratch) + grid_bytes);
+    int* flags = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + 2 * grid_bytes);
+    CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)p.ctas * sizeof(int), st));
+    int h = p.h;
+    int pois = poison ? 1 : 0;
+    void* args[] = {(void*)&d_in, (void*)&d_out, (void*)&xb0, (void*)&xb1, (void*)&flags,
+                    (void*)&pitch, (void*)&nx, (void*)&ny, (void*)&wt, (void*)&steps,
+                    (void*)&h, (void*)&pois, (void*)&geo};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(p.ctas), dim3(threads), args,
+                                         (size_t)smem, st));
+    g_launches += 1;
+    CUDA_TRY(cudaGetLastError());
+    return DTB_OK;
+  }
+  // streaming passes, ping-ponging dst between out and a scratch grid
+  auto kern = stream_kernel<T, K, DYN>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int64_t passes = (steps + p.h - 1) / p.h;
+  T* tmp = nullptr;
+  if (passes > 1) {
+    void* scratch = nullptr;
+    std::lock_guard<std::mutex> lk(g_mu);
+    int rc = arena_get(g_scratch[device & 15], grid_bytes, &scratch);
+    if (rc) return rc;
+    tmp = reinterpret_cast<T*>(scratch);
+  }
+  const T* src = d_in;
+  int64_t done = 0;
+  for (int64_t i = 0; i < passes; ++i) {
+    const int s = (int)std::min<int64_t>(p.h, steps - done);
+    T* dst = ((passes - 1 - i) % 2 == 0) ? d_out : tmp;
+    kern<<<p.ctas, threads, smem, st>>>(src, dst, pitch, nx, ny, wt, s, poison ? 1 : 0, geo);
+    g_launches += 1;
+    CUDA_TRY(cudaGetLastError());
+    src = dst;
+    done += s;
+  }
+  return DTB_OK;
+}
+
+template <typename T>
+int dispatch(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch, int nx,
+             int ny, const Weights<T>& wt, int64_t steps, bool poison, cudaStream_t st) {
+  const bool dyn = p.dyn();
+  if constexpr (sizeof(T) == 8) {
+    if (p.K == 4) return dyn ? launch_plan_kernels<T, 4, true>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st)
+                             : launch_plan_kernels<T, 4, false>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st);
+    if (p.K == 8) return dyn ? launch_plan_kernels<T, 8, true>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st)
+                             : launch_plan_kernels<T, 8, false>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st);
+  } else {
+    if (p.K == 8) return dyn ? launch_plan_kernels<T, 8, true>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st)
+                             : launch_plan_kernels<T, 8, false>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st);
+    if (p.K == 16) return dyn ? launch_plan_kernels<T, 16, true>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st)
+                              : launch_plan_kernels<T, 16, false>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st);
+  }
+  return fail(DTB_EINFEASIBLE, "no kernel instance for elem %d K %d", (int)sizeof(T), p.K);
+}
+
+int validate(int64_t nx, int64_t ny, int64_t pitch, const double w[5], int64_t total_steps,
+             int64_t t_depth, const dtb_rect* valid) {
+  if (nx < 1 || ny < 1) return fail(DTB_EINVAL, "grid dims must be at least 1x1, got %lldx%lld", (long long)nx, (long long)ny);
+  if (pitch < nx + 2) return fail(DTB_EINVAL, "pitch %lld smaller than nx+2 = %lld", (long long)pitch, (long long)(nx + 2));
+  for (int i = 0; i < 5; ++i)
+    if (!std::isfinite(w[i])) return fail(DTB_EINVAL, "non-finite stencil weight %c=%g", "wescn"[i], w[i]);
+  if (t_depth < 1) return fail(DTB_EINVAL, "t_depth must be at least 1, got %lld", (long long)t_depth);
+  if (total_steps < 1 || total_steps % t_depth)
+    return fail(DTB_EINVAL, "total_steps %lld is not a positive multiple of t_depth %lld",
+                (long long)total_steps, (long long)t_depth);
+  if (valid) {
+    if (valid->width < 0 || valid->height < 0)
+      return fail(DTB_EINVAL, "negative rect dims: %lldx%lld", (long long)valid->width, (long long)valid->height);
+    if (valid->width == 0 || valid->height == 0 || valid->x0 < 0 || valid->y0 < 0 ||
+        valid->x0 + valid->width > nx || valid->y0 + valid->height > ny)
+      return fail(DTB_EINVAL, "valid region (%lld, %lld, %lld, %lld) not within domain %lldx%lld",
+                  (long long)valid->x0, (long long)valid->y0, (long long)valid->width,
+                  (long long)valid->height, (long long)nx, (long long)ny);
+  }
+  return DTB_OK;
+}
+
+void fill_report(const Plan& p, int64_t nx, int64_t ny, int64_t steps, int elem, dtb_report* rep) {
+  if (!rep) return;
+  memset(rep, 0, sizeof *rep);
+  rep->elem_bytes = elem;
+  rep->useful_compute_cells = nx * ny * steps;
+  if (p.mode == 2) {
+    rep->global_load_cells = nx * ny * steps;
+    rep->global_store_cells = nx * ny * steps;
+    return;
+  }
+  const int64_t passes = (steps + p.h - 1) / p.h;
+  int64_t load = 0, owned = nx * ny, halo_ring = 0;
+  for (int i = 0; i < p.sx.n; ++i)
+    for (int j = 0; j < p.sy.n; ++j) {
+      const int64_t lw = p.sx.l1[i] - p.sx.l0[i], lh = p.sy.l1[j] - p.sy.l0[j];
+      // domain cells of the load region (the ghost ring is not counted, metrics.py:3-6)
+      const int64_t dw = std::min<int64_t>(p.sx.l1[i], nx) - std::max(p.sx.l0[i], 0);
+      const int64_t dh = std::min<int64_t>(p.sy.l1[j], ny) - std::max(p.sy.l0[j], 0);
+      load += dw * dh;
+      halo_ring += dw * dh - (int64_t)(p.sx.o1[i] - p.sx.o0[i]) * (p.sy.o1[j] - p.sy.o0[j]);
+      (void)lw; (void)lh;
+    }
+  if (p.mode == 0) {
+    rep->global_load_cells = load + (passes - 1) * halo_ring;
+    rep->global_store_cells = owned + (passes - 1) * halo_ring;
+    rep->halo_exchanged_cells = (passes - 1) * halo_ring;
+  } else {
+    rep->global_load_cells = passes * load;
+    rep->global_store_cells = passes * owned;
+    rep->halo_exchanged_cells = 0;
+  }
+  rep->redundant_compute_cells = p.computed_cells_per_step * steps - nx * ny * steps;
+  rep->scratchpad_peak_bytes = p.smem_bytes;
+}
+
+template <typename T>
+int solve_dev(const T* d_in, T* d_out, int64_t nx, int64_t ny, int64_t pitch, const T w[5],
+              int64_t total_steps, int64_t t_depth, const dtb_rect* valid, unsigned flags,
+              cudaStream_t st, dtb_report* rep) {
+  double wd[5];
+  for (int i = 0; i < 5; ++i) wd[i] = (double)w[i];
+  int rc = validate(nx, ny, pitch, wd, total_steps, t_depth, valid);
+  if (rc) return rc;
+  if (d_in == d_out) return fail(DTB_EINVAL, "input and output buffers alias");
+  g_launches = 0;
+  // valid-region runs: frozen cells outside `valid` are carried by a plain
+  // copy, and the valid rectangle evolves as a standalone problem whose ghost
+  // ring is the surrounding frozen cells (engine.py:26-30, grid.py:199-222).
+  int64_t vx = 0, vy = 0, vnx = nx, vny = ny;
+  if (valid && !(valid->x0 == 0 && valid->y0 == 0 && valid->width == nx && valid->height == ny)) {
+    CUDA_TRY(cudaMemcpyAsync(d_out, d_in, (size_t)(ny + 2) * pitch * sizeof(T),
+                             cudaMemcpyDeviceToDevice, st));
+    vx = valid->x0; vy = valid->y0; vnx = valid->width; vny = valid->height;
+  }
+  const T* in_v = d_in + vy * pitch + vx;
+  T* out_v = d_out + vy * pitch + vx;
+  DevInfo dev;
+  rc = query_dev(dev);
+  if (rc) return rc;
+  int force = (flags & DTB_FLAG_FORCE_NAIVE) ? 2 : (flags & DTB_FLAG_FORCE_STREAM) ? 1 : 0;
+  int depth = (flags & DTB_FLAG_FORCE_DEPTH) ? (int)t_depth : 0;
+  Plan p;
+  char err[512];
+  if (!make_plan(vnx, vny, (int)sizeof(T), total_steps, dev, force, depth, p, err, sizeof err))
+    return fail(DTB_EINFEASIBLE, "%s", err);
+  const Weights<T> wt = to_weights<T>(w);
+  if (p.mode == 2) {
+    // naive: total_steps launches ping-ponging between out and scratch
+    const size_t grid_bytes = (size_t)(ny + 2) * pitch * sizeof(T);
+    T* tmp = nullptr;
+    if (total_steps > 1) {
+      void* s = nullptr;
+      int device;
+      CUDA_TRY(cudaGetDevice(&device));
+      std::lock_guard<std::mutex> lk(g_mu);
+      rc = arena_get(g_scratch[device & 15], grid_bytes, &s);
+      if (rc) return rc;
+      tmp = reinterpret_cast<T*>(s);
+      if (valid) CUDA_TRY(cudaMemcpyAsync(tmp, d_in, grid_bytes, cudaMemcpyDeviceToDevice, st));
+    }
+    T* tmp_v = tmp ? tmp + vy * pitch + vx : nullptr;
+    const T* src = in_v;
+    dim3 block(256), grid((unsigned)((vnx + 2 + 255) / 256), (unsigned)std::min<int64_t>(vny + 2, 65535));
+    for (int64_t i = 0; i < total_steps; ++i) {
+      T* dst = ((total_steps - 1 - i) % 2 == 0) ? out_v : tmp_v;
+      naive_kernel<T><<<grid, block, 0, st>>>(src, dst, pitch, (int)vnx, (int)vny, wt);
+      g_launches += 1;
+      src = dst;
+    }
+    CUDA_TRY(cudaGetLastError());
+  } else {
+    Geometry geo;
+    rc = fill_geometry(p, geo);
+    if (rc) return rc;
+    rc = dispatch<T>(p, geo, in_v, out_v, pitch, (int)vnx, (int)vny, wt, total_steps,
+                     (flags & DTB_FLAG_POISON) != 0, st);
+    if (rc) return rc;
+  }
+  fill_report(p, vnx, vny, total_steps, (int)sizeof(T), rep);
+  return DTB_OK;
+}
+
+template <typename T>
+int solve_host(const T* in, T* out, int64_t nx, int64_t ny, int64_t pitch, const T w[5],
+               int64_t total_steps, int64_t t_depth, const dtb_rect* valid, int ilp, int n_gpus,
+               unsigned flags, dtb_report* rep) {
+  if (!in || !out) return fail(DTB_EINVAL, "null buffer");
+  if (ilp < 1) return fail(DTB_EINVAL, "ilp must be at least 1, got %d", ilp);
+  if (n_gpus != 1) return fail(DTB_EINVAL, "n_gpus=%d: the host entry point drives one GPU; use the slab API for more", n_gpus);
+  double wd[5];
+  for (int i = 0; i < 5; ++i) wd[i] = (double)w[i];
+  int rc = validate(nx, ny, pitch, wd, total_steps, t_depth, valid);
+  if (rc) return rc;
+  int device;
+  CUDA_TRY(cudaGetDevice(&device));
+  const size_t bytes = (size_t)(ny + 2) * pitch * sizeof(T);
+  void* io = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    rc = arena_get(g_io[device & 15], 2 * bytes, &io);
+    if (rc) return rc;
+  }
+  T* d_in = reinterpret_cast<T*>(io);
+  T* d_out = reinterpret_cast<T*>(reinterpret_cast<char*>(io) + bytes);
+  cudaStream_t st = 0;
+  CUDA_TRY(cudaMemcpyAsync(d_in, in, bytes, cudaMemcpyHostToDevice, st));
+  rc = solve_dev<T>(d_in, d_out, nx, ny, pitch, w, total_steps, t_depth, valid, flags, st, rep);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return DTB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dtb_j2d5pt_f64(const double* in, double* out, int64_t nx, int64_t ny, int64_t pitch,
+                   const double w[5], int64_t total_steps, int64_t t_depth,
+                   const dtb_rect* valid, int ilp, int n_gpus, unsigned flags,
+                   dtb_report* rep) {
+  g_err.clear();
+  return solve_host<double>(in, out, nx, ny, pitch, w, total_steps, t_depth, valid, ilp, n_gpus,
+                            flags, rep);
+}
+
+int dtb_j2d5pt_f32(const float* in, float* out, int64_t nx, int64_t ny, int64_t pitch,
+                   const float w[5], int64_t total_steps, int64_t t_depth,
+                   const dtb_rect* valid, int ilp, int n_gpus, unsigned flags,
+                   dtb_report* rep) {
+  g_err.clear();
+  return solve_host<float>(in, out, nx, ny, pitch, w, total_steps, t_depth, valid, ilp, n_gpus,
+                           flags, rep);
+}
+
+int dtb_j2d5pt_f64_dev(const double* d_in, double* d_out, int64_t nx, int64_t ny,
+                       int64_t pitch, const double w[5], int64_t total_steps,
+                       int64_t t_depth, const dtb_rect* valid, unsigned flags,
+                       void* stream, dtb_report* rep) {
+  g_err.clear();
+  return solve_dev<double>(d_in, d_out, nx, ny, pitch, w, total_steps, t_depth, valid, flags,
+                           (cudaStream_t)stream, rep);
+}
+
+int dtb_j2d5pt_f32_dev(const float* d_in, float* d_out, int64_t nx, int64_t ny,
+                       int64_t pitch, const float w[5], int64_t total_steps,
+                       int64_t t_depth, const dtb_rect* valid, unsigned flags,
+                       void* stream, dtb_report* rep) {
+  g_err.clear();
+  return solve_dev<float>(d_in, d_out, nx, ny, pitch, w, total_steps, t_depth, valid, flags,
+                          (cudaStream_t)stream, rep);
+}
+
+int dtb_plan(int64_t nx, int64_t ny, int32_t elem_bytes, int64_t total_steps, int64_t t_depth,
+             unsigned flags, dtb_plan_info* out) {
+  g_err.clear();
+  if (!out) return fail(DTB_EINVAL, "null plan output");
+  if (elem_bytes != 4 && elem_bytes != 8) return fail(DTB_EINVAL, "elem_bytes must be 4 or 8, got %d", elem_bytes);
+  DevInfo dev;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0) {
+    int rc = query_dev(dev);
+    if (rc) return rc;
+  } else {
+    cudaGetLastError();  // no GPU: plan for the B200 defaults (148 SMs, 227 KB)
+  }
+  int force = (flags & DTB_FLAG_FORCE_NAIVE) ? 2 : (flags & DTB_FLAG_FORCE_STREAM) ? 1 : 0;
+  int depth = (flags & DTB_FLAG_FORCE_DEPTH) ? (int)t_depth : 0;
+  Plan p;
+  char err[512];
+  if (!make_plan(nx, ny, elem_bytes, total_steps, dev, force, depth, p, err, sizeof err))
+    return fail(DTB_EINFEASIBLE, "%s", err);
+  memset(out, 0, sizeof *out);
+  out->mode = p.mode;
+  out->elem_bytes = elem_bytes;
+  out->lane_elems = p.K;
+  out->warps = p.warps;
+  out->halo = p.h;
+  out->tiles_x = p.sx.n;
+  out->tiles_y = p.sy.n;
+  out->ctas = p.ctas;
+  out->ctas_per_sm = p.ctas_per_sm;
+  out->dyn = p.dyn() ? 1 : 0;
+  out->smem_bytes = p.smem_bytes;
+  for (int i = 0; i < p.sx.n; ++i) {
+    out->tile_w = std::max<int64_t>(out->tile_w, p.sx.o1[i] - p.sx.o0[i]);
+    out->load_w = std::max<int64_t>(out->load_w, p.sx.l1[i] - p.sx.l0[i]);
+  }
+  for (int j = 0; j < p.sy.n; ++j) {
+    out->tile_h = std::max<int64_t>(out->tile_h, p.sy.o1[j] - p.sy.o0[j]);
+    out->load_h = std::max<int64_t>(out->load_h, p.sy.l1[j] - p.sy.l0[j]);
+  }
+  out->computed_cells_per_step = p.computed_cells_per_step;
+  out->est_cells_per_clk = p.cells_per_clk;
+  return DTB_OK;
+}
+
+int64_t dtb_last_launch_count(void) { return g_launches; }
+
+int dtb_device_info(int32_t* sms, int64_t* smem_optin_per_block, int64_t* l2_bytes,
+                    int32_t* cc_major, int32_t* cc_minor) {
+  g_err.clear();
+  DevInfo d;
+  int rc = query_dev(d);
+  if (rc) return rc;
+  int dev = 0, maj = 0, mnr = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&maj, cudaDevAttrComputeCapabilityMajor, dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&mnr, cudaDevAttrComputeCapabilityMinor, dev));
+  if (sms) *sms = d.sms;
+  if (smem_optin_per_block) *smem_optin_per_block = d.smem_optin;
+  if (l2_bytes) *l2_bytes = d.l2_bytes;
+  if (cc_major) *cc_major = maj;
+  if (cc_minor) *cc_minor = mnr;
+  return DTB_OK;
+}
+
+int dtb_fill_random_f64(double* d_out, int64_t nx, int64_t ny, int64_t pitch, uint64_t seed,
+                        double ghost, void* stream) {
+  g_err.clear();
+  if (nx < 1 || ny < 1 || pitch < nx + 2) return fail(DTB_EINVAL, "bad fill dims");
+  fill_random_kernel<double><<<1184, 256, 0, (cudaStream_t)stream>>>(d_out, pitch, (int)nx, (int)ny, seed, ghost);
+  CUDA_TRY(cudaGetLastError());
+  return DTB_OK;
+}
+
+int dtb_fill_random_f32(float* d_out, int64_t nx, int64_t ny, int64_t pitch, uint64_t seed,
+                        double ghost, void* stream) {
+  g_err.clear();
+  if (nx < 1 || ny < 1 || pitch < nx + 2) return fail(DTB_EINVAL, "bad fill dims");
+  fill_random_kernel<float><<<1184, 256, 0, (cudaStream_t)stream>>>(d_out, pitch, (int)nx, (int)ny, seed, ghost);
+  CUDA_TRY(cudaGetLastError());
+  return DTB_OK;
+}
+
+const char* dtb_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,255 @@
+// dtb_plan.cpp — B200 tile planner; see dtb_plan.h for the model.
+#include "dtb_plan.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+
+namespace dtb {
+
+bool make_split(int N, int n, int h, int align, int maxL, int min_owned, Split& s) {
+  s = Split();
+  if (n < 1 || N < 1) return false;
+  s.n = n;
+  s.o0.resize(n); s.o1.resize(n); s.l0.resize(n); s.l1.resize(n);
+  std::vector<int> left(n), right(n);
+  long S = N;
+  for (int i = 0; i < n; ++i) {
+    left[i] = (i == 0) ? 1 : h;
+    right[i] = (i == n - 1) ? 1 : h;
+    S += left[i] + right[i];
+  }
+  // equal load extents: the per-CTA cost is set by the load region
+  const long Lt = S / n, rem = S % n;
+  int x = 0;
+  for (int i = 0; i < n; ++i) {
+    long own = Lt + (i < rem ? 1 : 0) - left[i] - right[i];
+    if (own < std::max(1, min_owned)) return false;
+    s.o0[i] = x;
+    s.o1[i] = x + (int)own;
+    x += (int)own;
+  }
+  if (x != N) return false;
+  for (int i = 0; i < n; ++i) {
+    s.l0[i] = std::max(s.o0[i] - left[i], -1);
+    s.l1[i] = std::min(s.o1[i] + right[i], N + 1);
+  }
+  for (int i = 0; i < n; ++i) {
+    int L = s.l1[i] - s.l0[i];
+    int ext = (align - L % align) % align;
+    if (ext) {
+      // grow the halo into a neighbour (never beyond that neighbour's owned cells)
+      int rlim = (i + 1 < n) ? s.o1[i + 1] : N + 1;
+      int take = std::min(ext, rlim - s.l1[i]);
+      s.l1[i] += take;
+      ext -= take;
+      int llim = (i > 0) ? s.o0[i - 1] : -1;
+      take = std::min(ext, s.l0[i] - llim);
+      s.l0[i] -= take;
+      ext -= take;
+      if (ext) s.dyn = true;
+    }
+    s.max_load = std::max(s.max_load, s.l1[i] - s.l0[i]);
+  }
+  return s.max_load <= maxL;
+}
+
+namespace {
+
+struct Shape { int K; int warps; };
+
+double lanes_per_clk(int elem) { return elem == 8 ? 64.0 : 128.0; }
+// FP32 is issue-bound (FADD/FMUL alone fill the 4 issue slots per SM per
+// clock), so the non-FP instructions per row cost throughput there.
+double fp_efficiency(int elem) { return elem == 8 ? 0.92 : 0.80; }
+
+// SM cycles for one CTA to advance a (Lw x Lh) tile by `steps` steps.
+double tile_cycles(int elem, int K, int warps, int Lh, int steps) {
+  const int rows = Lh - 2;
+  if (rows <= 0 || steps <= 0) return 0;
+  const double row_cost = 32.0 * K * 9.0 / (lanes_per_clk(elem) * fp_efficiency(elem));
+  double cyc = 0;
+  int s = steps;
+  if (s >= 2 && rows >= 2) {
+    const int nb = std::max(1, std::min(warps, rows / 2));
+    const int hb = (rows + nb - 1) / nb;
+    // each band: hb level-1 rows + 2 redundant seam rows + hb level-2 rows
+    const double sweep = nb * (2.0 * hb + 2.0) * row_cost + 400.0;  // + 2 barriers, fill
+    cyc += (s / 2) * sweep;
+    s %= 2;
+  }
+  if (s) {
+    const int nb = std::max(1, std::min(warps, rows));
+    const int hb = (rows + nb - 1) / nb;
+    cyc += s * (nb * (double)hb * row_cost + 300.0);
+  }
+  return cyc;
+}
+
+// sustained HBM bytes per SM clock (6545 GB/s measured copy, ~1.9 GHz)
+constexpr double kHbmBytesPerClk = 3400.0;
+// L2 bytes per clock for the resident halo exchange and epoch handshake
+constexpr double kL2BytesPerClk = 5000.0;
+constexpr double kExchangeLatency = 3500.0;  // flag publish + neighbour poll (~2 x 0.48 us)
+
+bool plan_resident(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& dev,
+                   int depth, Plan& best) {
+  bool found = false;
+  const Shape shapes8[] = {{4, 16}, {8, 8}};
+  const Shape shapes4[] = {{8, 16}, {16, 8}};
+  const Shape* shapes = elem == 8 ? shapes8 : shapes4;
+  for (int si = 0; si < 2; ++si) {
+    const int K = shapes[si].K, W = shapes[si].warps;
+    const int Lw_max = 32 * K;
+    const int64_t row_bytes = (int64_t)Lw_max * elem;
+    const int maxRows = (int)((dev.smem_optin - 1024) / row_bytes);
+    if (maxRows < 3) continue;
+    for (int h = 2; h <= 32; h += 2) {
+      if (depth > 0 && h != depth) continue;
+      const int hh = (int)std::min<int64_t>(h, std::max<int64_t>(steps, 1));
+      const int ntx_min = (int)((nx + 2 + Lw_max - 1) / Lw_max);
+      for (int ntx = std::max(1, ntx_min); ntx <= std::min<int64_t>(dev.sms, nx); ++ntx) {
+        Split sx;
+        if (!make_split((int)nx, ntx, h, K, Lw_max, ntx > 1 ? h : 1, sx)) continue;
+        const int nty_max = (int)std::min<int64_t>(dev.sms / ntx, ny);
+        for (int nty = nty_max; nty >= std::max(1, nty_max - 2); --nty) {
+          Split sy;
+          if (!make_split((int)ny, nty, h, 1, maxRows, nty > 1 ? h : 1, sy)) continue;
+          // cost per epoch of hh steps: slowest CTA + exchange
+          double cyc = tile_cycles(elem, K, W, sy.max_load, hh);
+          if (steps > hh) {
+            const double band = 2.0 * h * (sx.max_load + sy.max_load) * elem;  // write + read
+            cyc += kExchangeLatency + 2.0 * band * dev.sms / kL2BytesPerClk;
+          }
+          const double per_step = cyc / hh;
+          const double cpc = (double)nx * ny / per_step;
+          if (!found || cpc > best.cells_per_clk) {
+            found = true;
+            best.mode = 0;
+            best.elem = elem;
+            best.K = K;
+            best.warps = W;
+            best.h = h;
+            best.sx = sx;
+            best.sy = sy;
+            best.ctas = ntx * nty;
+            best.ctas_per_sm = 1;
+            best.smem_bytes = (int64_t)sy.max_load * row_bytes;
+            best.cycles_per_step = per_step;
+            best.cells_per_clk = cpc;
+          }
+        }
+        if (sx.max_load < Lw_max / 2 && ntx > ntx_min) break;
+      }
+    }
+  }
+  return found;
+}
+
+bool plan_streaming(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& dev,
+                    int depth, Plan& best) {
+  bool found = false;
+  const Shape shapes8[] = {{4, 16}, {8, 8}};
+  const Shape shapes4[] = {{8, 16}, {16, 8}};
+  const Shape* shapes = elem == 8 ? shapes8 : shapes4;
+  for (int si = 0; si < 2; ++si) {
+    const int K = shapes[si].K, W = shapes[si].warps;
+    const int Lw_max = 32 * K;
+    const int64_t row_bytes = (int64_t)Lw_max * elem;
+    for (int occ = 1; occ <= 2; ++occ) {
+      const int64_t smem_cta = std::min<int64_t>(dev.smem_optin, dev.smem_per_sm / occ - 1024);
+      const int maxRows = (int)((smem_cta - 1024) / row_bytes);
+      if (maxRows < 8) continue;
+      for (int h = 2; h <= 32; h += 2) {
+        if (depth > 0 && h != depth) continue;
+        const int hh = (int)std::min<int64_t>(h, std::max<int64_t>(steps, 1));
+        const int ntx_min = (int)((nx + 2 + Lw_max - 1) / Lw_max);
+        for (int ntx = std::max(1, ntx_min); ntx <= ntx_min + 2 && ntx <= nx; ++ntx) {
+          Split sx;
+          if (!make_split((int)nx, ntx, h, K, Lw_max, 1, sx)) continue;
+          // tallest tiles that fit
+          int nty = (int)std::max<int64_t>(1, (ny + 2 + maxRows - 1) / maxRows);
+          Split sy;
+          for (; nty <= ny; ++nty)
+            if (make_split((int)ny, nty, h, 1, maxRows, 1, sy)) break;
+          if (nty > ny) continue;
+          const int64_t ntiles = (int64_t)ntx * nty;
+          const int64_t slots = (int64_t)dev.sms * occ;
+          const double waves = std::ceil((double)ntiles / slots);
+          const double tc = tile_cycles(elem, K, W, sy.max_load, hh);
+          const double load_b = (double)sx.max_load * sy.max_load * elem;
+          const double store_b = (double)(sx.max_load - 2 * h) * (sy.max_load - 2 * h) * elem;
+          // per-CTA memory time at its share of HBM bandwidth
+          const double mem_cta = (load_b + store_b) / (kHbmBytesPerClk / slots);
+          // a wave = occ tiles per SM sharing its FP pipe; one CTA's load/store
+          // overlaps the other CTAs' compute when occ >= 2
+          const double pass = waves * std::max(occ * tc, mem_cta + tc) + 6000.0;
+          const double per_step = pass / hh;
+          const double cpc = (double)nx * ny / per_step;
+          if (!found || cpc > best.cells_per_clk) {
+            found = true;
+            best.mode = 1;
+            best.elem = elem;
+            best.K = K;
+            best.warps = W;
+            best.h = h;
+            best.sx = sx;
+            best.sy = sy;
+            best.ctas = (int)std::min<int64_t>(ntiles, slots);
+            best.ctas_per_sm = occ;
+            best.smem_bytes = (int64_t)sy.max_load * row_bytes;
+            best.cycles_per_step = per_step;
+            best.cells_per_clk = cpc;
+          }
+        }
+      }
+    }
+  }
+  return found;
+}
+
+}  // namespace
+
+bool make_plan(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& dev, int force,
+               int depth, Plan& out, char* err, int errlen) {
+  if (nx < 1 || ny < 1) {
+    snprintf(err, errlen, "domain dims must be at least 1x1, got %lldx%lld", (long long)nx,
+             (long long)ny);
+    return false;
+  }
+  if (nx > (1 << 30) || ny > (1 << 30)) {
+    snprintf(err, errlen, "domain %lldx%lld too large", (long long)nx, (long long)ny);
+    return false;
+  }
+  Plan p;
+  bool ok = false;
+  if (force == 2) {
+    p.mode = 2;
+    p.elem = elem;
+    p.h = 1;
+    ok = true;
+  } else {
+    if (force == 0) ok = plan_resident(nx, ny, elem, steps, dev, depth, p);
+    if (!ok) ok = plan_streaming(nx, ny, elem, steps, dev, depth, p);
+  }
+  if (!ok) {
+    snprintf(err, errlen,
+             "no B200 tiling fits %lldx%lld (elem %d B, depth %d) in %lld B of shared memory per CTA",
+             (long long)nx, (long long)ny, elem, depth, (long long)dev.smem_optin);
+    return false;
+  }
+  // lane-cells updated per step (every inner cell of every load region)
+  int64_t computed = 0;
+  if (p.mode == 2) {
+    computed = nx * ny;
+  } else {
+    for (int i = 0; i < p.sx.n; ++i)
+      for (int j = 0; j < p.sy.n; ++j)
+        computed += (int64_t)(p.sx.l1[i] - p.sx.l0[i] - 2) * (p.sy.l1[j] - p.sy.l0[j] - 2);
+  }
+  p.computed_cells_per_step = computed;
+  out = p;
+  return true;
+}
+
+}  // namespace dtb

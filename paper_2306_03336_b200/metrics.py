@@ -1,0 +1,86 @@
+"""Traffic accounting (mirrors dtb.metrics' TrafficReport and models, metrics.py:39-126).
+
+``run_dtb`` returns a :class:`TrafficReport`. When the caller passes a
+reference-style :class:`~.planner.TilingPlan`, the report is that plan's
+analytic model — exactly the counters the reference engine reconciles to
+(``report == model_dtb_traffic(plan, steps, valid)``, test_engine.py:41-50).
+The B200 schedule's own traffic is returned by ``run_dtb_b200`` as a
+:class:`TrafficReport` filled from the native plan (dtb_report).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from .grid import Rect
+from .planner import DEFAULT_ELEM_BYTES, tile_active_region
+
+__all__ = ["TrafficReport", "model_naive_traffic", "model_dtb_traffic"]
+
+
+@dataclass(frozen=True)
+class TrafficReport:
+    global_load_cells: int
+    global_store_cells: int
+    halo_exchanged_cells: int
+    redundant_compute_cells: int
+    useful_compute_cells: int
+    scratchpad_peak_bytes: int
+    elem_bytes: int = DEFAULT_ELEM_BYTES
+
+    @property
+    def global_load_bytes(self) -> int:
+        return self.global_load_cells * self.elem_bytes
+
+    @property
+    def global_store_bytes(self) -> int:
+        return self.global_store_cells * self.elem_bytes
+
+    @property
+    def halo_exchanged_bytes(self) -> int:
+        return self.halo_exchanged_cells * self.elem_bytes
+
+    @property
+    def traffic_cells(self) -> int:
+        return self.global_load_cells + self.global_store_cells
+
+
+def model_naive_traffic(domain, steps: int, elem_bytes: int = DEFAULT_ELEM_BYTES) -> TrafficReport:
+    """One load + one store per cell per step (metrics.py:69-86)."""
+    nx, ny = domain
+    if nx < 0 or ny < 0:
+        raise ValueError(f"negative domain dims {domain}")
+    if steps < 0:
+        raise ValueError(f"negative steps {steps}")
+    n = nx * ny * steps
+    return TrafficReport(n, n, 0, 0, n, 0, elem_bytes)
+
+
+def model_dtb_traffic(plan, total_steps: int, valid=None) -> TrafficReport:
+    """Counters of the reference schedule for ``plan`` (metrics.py:89-126):
+    per time block, every tile loads its load region's domain cells and
+    stores its interior; 2*(active workers-1) halo columns of the domain rows
+    per superstep; compute = the trapezoid areas."""
+    if total_steps < 1 or total_steps % plan.t_depth:
+        raise ValueError(f"total_steps {total_steps} is not a positive multiple of "
+                         f"t_depth {plan.t_depth}")
+    domain = Rect(0, 0, plan.nx, plan.ny)
+    if valid is None:
+        valid = domain
+    elif not domain.contains(valid) or valid.width == 0 or valid.height == 0:
+        raise ValueError(f"valid region {valid} not within domain {domain}")
+    blocks = total_steps // plan.t_depth
+    loads = stores = halo = compute = 0
+    for tile in plan.tiles:
+        lr = tile.load_region
+        covered = domain.intersect(lr)
+        loads += covered.area
+        stores += tile.interior.width * tile.interior.height
+        active = min(plan.device.workers, lr.width)
+        halo += 2 * max(active - 1, 0) * covered.height * plan.t_depth
+        compute += sum(tile_active_region(tile, s, valid).area
+                       for s in range(1, plan.t_depth + 1))
+    useful = valid.width * valid.height * total_steps
+    return TrafficReport(loads * blocks, stores * blocks, halo * blocks,
+                         compute * blocks - useful, useful, plan.footprint_bytes,
+                         plan.elem_bytes)

@@ -1,0 +1,50 @@
+"""Seeded synthetic inputs (the reference's portable generator, prng.py:45-67).
+
+``random_interior(nx, ny, seed)`` yields the same bits as the reference's
+counter-mode splitmix64 fill; ``fill_random_device`` produces them directly
+in HBM through the native kernel (dtb_fill_random_*), so 32768^2 inputs need
+no host fill or H2D copy.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+__all__ = ["splitmix64", "random_doubles", "random_interior", "fill_random_device"]
+
+_GOLDEN = np.uint64(0x9E3779B97F4B7C15)
+_M1 = np.uint64(0xBF58476D1CE4E5B9)
+_M2 = np.uint64(0x94D049BB133111EB)
+
+
+def splitmix64(seed: int, n: int) -> np.ndarray:
+    if n < 0:
+        raise ValueError("n must be non-negative")
+    z = np.uint64(seed & (2 ** 64 - 1)) + np.arange(1, n + 1, dtype=np.uint64) * _GOLDEN
+    z = (z ^ (z >> np.uint64(30))) * _M1
+    z = (z ^ (z >> np.uint64(27))) * _M2
+    return z ^ (z >> np.uint64(31))
+
+
+def random_doubles(seed: int, n: int) -> np.ndarray:
+    return (splitmix64(seed, n) >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+
+
+def random_interior(nx: int, ny: int, seed: int) -> np.ndarray:
+    return random_doubles(seed, nx * ny).reshape(ny, nx)
+
+
+def fill_random_device(buf, nx: int, ny: int, seed: int, ghost: float = 0.0, stream=None):
+    """Fill a padded (ny+2, pitch) CUDA tensor like grid_new(nx, ny, random_interior(...), ghost)."""
+    import torch
+    from . import _native
+    if stream is None:
+        stream = torch.cuda.current_stream(buf.device).cuda_stream
+    fn = _native.lib().dtb_fill_random_f64 if buf.dtype == torch.float64 else \
+        _native.lib().dtb_fill_random_f32
+    rc = fn(buf.data_ptr(), nx, ny, buf.stride(0), seed & (2 ** 64 - 1), float(ghost),
+            ctypes.c_void_p(stream))
+    if rc != 0:
+        raise RuntimeError(_native.last_error())

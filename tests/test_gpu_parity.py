@@ -1,0 +1,215 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden outputs and the pinned CPU oracle — bit for bit, every mode.
+
+Tolerance: none. Every comparison is on the uint64/uint32 bit patterns
+(the reference's grid_compare contract, grid.py:238-256); the FMA-free
+W,E,S,C,N update makes the B200 schedules bitwise equal to jacobi_reference
+for fp64, and to the fp32 restatement for fp32.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import jacobi_c, jacobi_numpy
+from paper_2306_03336_b200 import (DeviceModel, Grid2D, KernelConfig, Rect, StencilWeights, grid_extract,
+                                   grid_new, j2d5pt, last_launch_count, plan_device_tiles, run_dtb,
+                                   run_dtb_b200)
+from paper_2306_03336_b200 import _native
+from paper_2306_03336_b200.prng import random_interior
+
+pytestmark = pytest.mark.gpu
+
+W02 = StencilWeights.diffusive(0.2)
+MIXED = StencilWeights(0.11, -0.2, 0.37, 0.5, -0.07)
+STREAM, NAIVE = _native.FLAG_FORCE_STREAM, _native.FLAG_FORCE_NAIVE
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint64 if a.dtype == np.float64 else np.uint32)
+
+
+def same(a, b):
+    return np.array_equal(bits(a), bits(b))
+
+
+def rgrid(nx, ny, seed=0, ghost=0.0):
+    return grid_new(nx, ny, random_interior(nx, ny, seed), ghost=ghost)
+
+
+def test_kats_and_random_golden(golden):
+    _, arr = golden
+    steps = {"kat_spike1": 1, "kat_spike2": 2, "kat_drift": 1}
+    for name in ["kat_spike1", "kat_spike2", "kat_fixed0.25", "kat_fixed0.125", "kat_drift"]:
+        g = arr[f"{name}_in"]
+        out = j2d5pt(Grid2D(g.shape[1] - 2, g.shape[0] - 2, g), arr[f"{name}_w"],
+                     steps.get(name, 20))
+        assert same(out.data, arr[f"{name}_out"]), name
+    i = 0
+    while f"rand{i}_in" in arr:
+        g = arr[f"rand{i}_in"]
+        grid = Grid2D(g.shape[1] - 2, g.shape[0] - 2, g)
+        for flags in (0, STREAM, NAIVE):
+            out, _ = run_dtb_b200(grid, arr[f"rand{i}_w"], int(arr[f"rand{i}_steps"]), flags=flags)
+            assert same(out.data, arr[f"rand{i}_out"]), (i, flags)
+        i += 1
+
+
+def test_c1_matches_reference_hash(golden):
+    meta, _ = golden
+    for case in meta["cases"]:
+        if not case["name"].startswith("C1"):
+            continue
+        g = rgrid(case["nx"], case["ny"], case["seed"], case["ghost"])
+        for flags in (0, STREAM):
+            out, _ = run_dtb_b200(g, case["weights"], case["steps"], flags=flags)
+            assert sha(out.data) == case["sha256_out"], (case["name"], flags)
+        assert last_launch_count() >= 1
+
+
+def test_reference_batch_hashes(golden):
+    meta, _ = golden
+    for rec in meta["batch"]:
+        g = rgrid(rec["nx"], rec["ny"], rec["seed"])
+        out = j2d5pt(g, rec["weights"], rec["steps"])
+        assert sha(out.data) == rec["sha256_out"], rec
+
+
+def test_run_dtb_with_reference_plans(golden):
+    meta, arr = golden
+    for run in meta["runs"]:
+        g = arr[f"{run['key']}_in"]
+        grid = Grid2D(run["nx"], run["ny"], g)
+        plan = plan_device_tiles((run["nx"], run["ny"]), DeviceModel("d", run["workers"], run["cap"]),
+                                 run["t_depth"])
+        v = Rect(*run["valid"]) if run["valid"] else None
+        before = g.copy()
+        out, rep = run_dtb(grid, W02, run["steps"], plan, KernelConfig(4), valid=v)
+        assert same(out.data, arr[f"{run['key']}_out"]), run["key"]
+        assert [rep.global_load_cells, rep.global_store_cells, rep.halo_exchanged_cells,
+                rep.redundant_compute_cells, rep.useful_compute_cells,
+                rep.scratchpad_peak_bytes, rep.elem_bytes] == run["report"]
+        assert same(grid.data, before)  # input untouched
+
+
+def test_pruned_valid_region_acceptance_2(golden):
+    meta, _ = golden
+    case = next(c for c in meta["cases"] if c["name"] == "pruned_560x536")
+    g = rgrid(case["nx"], case["ny"], case["seed"])
+    v = Rect(*case["valid"])
+    for flags in (0, STREAM, NAIVE):
+        out, _ = run_dtb_b200(g, case["weights"], case["steps"], valid=v, flags=flags)
+        assert sha(grid_extract(out, v).data) == case["sha256_valid_out"], flags
+        mask = np.ones((case["ny"], case["nx"]), bool)
+        mask[v.y0:v.y1, v.x0:v.x1] = False
+        assert same(out.interior[mask], g.interior[mask])
+
+
+SHAPES = [(1, 1), (2, 2), (3, 7), (8, 8), (17, 5), (33, 29), (64, 64), (127, 130), (128, 126),
+          (129, 64), (255, 257), (300, 41), (41, 300), (600, 500)]
+
+
+@pytest.mark.parametrize("nx,ny", SHAPES)
+def test_modes_and_depths_match_oracle(nx, ny):
+    g = rgrid(nx, ny, nx * 1000 + ny, ghost=0.375)
+    for steps in (1, 2, 5, 12):
+        want = jacobi_c(g.data, MIXED.astuple(), steps)
+        for flags in (0, STREAM, NAIVE):
+            out, rep = run_dtb_b200(g, MIXED, steps, flags=flags)
+            assert same(out.data, want), (nx, ny, steps, flags)
+            assert rep.useful_compute_cells == nx * ny * steps
+        for depth in (2, 3, 6):
+            out, _ = run_dtb_b200(g, MIXED, steps, depth=depth)
+            assert same(out.data, want), (nx, ny, steps, "depth", depth)
+            out, _ = run_dtb_b200(g, MIXED, steps, depth=depth, flags=STREAM)
+            assert same(out.data, want), (nx, ny, steps, "stream depth", depth)
+
+
+@pytest.mark.parametrize("nx,ny", [(5, 5), (64, 48), (300, 257), (1000, 200)])
+def test_fp32_matches_fp32_oracle(nx, ny):
+    g = rgrid(nx, ny, 77, ghost=0.5)
+    for steps in (1, 4, 9):
+        want = jacobi_numpy(g.data, W02.astuple(), steps, np.float32)
+        for flags in (0, STREAM, NAIVE):
+            out, _ = run_dtb_b200(g, W02, steps, flags=flags, dtype=np.float32)
+            assert same(out.data.astype(np.float32), want), (nx, ny, steps, flags)
+
+
+def test_poison_mode_does_not_leak():
+    g = rgrid(129, 93, 7, ghost=1.5)
+    want = jacobi_c(g.data, W02.astuple(), 16)
+    for flags in (0, STREAM):
+        for depth in (2, 4, 8):
+            out, _ = run_dtb_b200(g, W02, 16, poison=True, flags=flags, depth=depth)
+            assert same(out.data, want), (flags, depth)
+            assert not np.isnan(out.data).any()
+
+
+def test_determinism_and_input_untouched():
+    g = rgrid(300, 300, 5)
+    before = g.data.copy()
+    a = j2d5pt(g, MIXED, 37)
+    b = j2d5pt(g, MIXED, 37)
+    assert same(a.data, b.data) and same(g.data, before)
+
+
+def test_zero_steps_copy_and_negative_steps():
+    g = rgrid(6, 5, 1, ghost=2.5)
+    assert same(j2d5pt(g, W02, 0).data, g.data)
+    with pytest.raises(ValueError):
+        j2d5pt(g, W02, -1)
+
+
+def test_c2_shape_resident_vs_oracle():
+    # BASELINE config C2 geometry (1900^2 fp64, resident), 64 steps
+    g = rgrid(1900, 1900, 1)
+    out, rep = run_dtb_b200(g, W02, 64)
+    assert same(out.data, jacobi_c(g.data, W02.astuple(), 64))
+    assert rep.scratchpad_peak_bytes <= 232448
+
+
+@pytest.mark.slow
+def test_c2_full_10000_steps_bitwise():
+    # the headline configuration, all 10^4 steps, against the C oracle
+    g = rgrid(1900, 1900, 1)
+    out, _ = run_dtb_b200(g, W02, 10000)
+    assert same(out.data, jacobi_c(g.data, W02.astuple(), 10000))
+
+
+def test_c3a_shape_fp32_resident_vs_oracle():
+    g = rgrid(2700, 2700, 1)
+    out, _ = run_dtb_b200(g, W02, 40, dtype=np.float32)
+    assert same(out.data.astype(np.float32), jacobi_c(g.data, W02.astuple(), 40, np.float32))
+
+
+def test_streaming_large_fp64_vs_oracle():
+    g = rgrid(4096, 3000, 3)
+    out, _ = run_dtb_b200(g, MIXED, 24)
+    assert same(out.data, jacobi_c(g.data, MIXED.astuple(), 24))
+
+
+def test_streaming_c3b_shape_fp32_vs_oracle():
+    g = rgrid(8192, 8192, 1)
+    out, _ = run_dtb_b200(g, W02, 12, dtype=np.float32)
+    assert same(out.data.astype(np.float32), jacobi_c(g.data, W02.astuple(), 12, np.float32))
+
+
+def test_device_tensor_entry_and_gpu_fill():
+    import torch
+    from paper_2306_03336_b200 import j2d5pt_device
+    from paper_2306_03336_b200.prng import fill_random_device
+    nx, ny = 777, 555
+    a = torch.empty((ny + 2, nx + 2), dtype=torch.float64, device="cuda")
+    b = torch.empty_like(a)
+    fill_random_device(a, nx, ny, 42, ghost=0.25)
+    host = rgrid(nx, ny, 42, ghost=0.25)
+    assert same(a.cpu().numpy(), host.data)
+    j2d5pt_device(a, b, nx, ny, MIXED, 33)
+    torch.cuda.synchronize()
+    assert same(b.cpu().numpy(), jacobi_c(host.data, MIXED.astuple(), 33))
