@@ -47,6 +47,7 @@ extern "C" {
 #define DTB_FLAG_FORCE_STREAM 2u    /* use the streaming (T-fused HBM pass) kernel even if resident fits */
 #define DTB_FLAG_FORCE_NAIVE 4u     /* one global-memory step per launch (the T=1 HBM baseline) */
 #define DTB_FLAG_FORCE_DEPTH 8u     /* use t_depth as the temporal halo depth instead of the planner's */
+#define DTB_FLAG_TRACE 16u          /* resident kernel: per-CTA clock64 phase counters (dtb_last_trace) */
 
 /* Half-open rectangle in interior coordinates (grid.py:38-92). */
 typedef struct dtb_rect {
@@ -111,6 +112,12 @@ int dtb_j2d5pt_f32_dev(const float* d_in, float* d_out, int64_t nx, int64_t ny,
 /* Plan without executing (the B200 analogue of plan_device_tiles). */
 int dtb_plan(int64_t nx, int64_t ny, int32_t elem_bytes, int64_t total_steps,
              int64_t t_depth, unsigned flags, dtb_plan_info* out);
+
+/* Phase counters of the most recent DTB_FLAG_TRACE resident solve on this
+ * thread: for each CTA, SM clock cycles spent in {compute, publish, wait,
+ * refresh} plus the epoch count (5 values per CTA). Copies up to n values
+ * into out and returns the number of CTAs (0 if no trace). */
+int64_t dtb_last_trace(int64_t* out, int64_t n);
 
 /* Kernel launches issued by the most recent solve on this thread. */
 int64_t dtb_last_launch_count(void);

@@ -25,6 +25,7 @@ FLAG_POISON = 1
 FLAG_FORCE_STREAM = 2
 FLAG_FORCE_NAIVE = 4
 FLAG_FORCE_DEPTH = 8
+FLAG_TRACE = 16
 
 
 class DtbRect(ctypes.Structure):
@@ -82,6 +83,7 @@ _SIGNATURES = {
     "dtb_plan": (c_int, [c_int64, c_int64, c_int32, c_int64, c_int64, c_uint,
                          POINTER(DtbPlanInfo)]),
     "dtb_last_launch_count": (c_int64, []),
+    "dtb_last_trace": (c_int64, [POINTER(c_int64), c_int64]),
     "dtb_device_info": (c_int, [POINTER(c_int32), POINTER(c_int64), POINTER(c_int64),
                                 POINTER(c_int32), POINTER(c_int32)]),
     "dtb_fill_random_f64": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_uint64, c_double,

@@ -81,35 +81,67 @@ struct Tile {
   }
 };
 
+// Per-lane shared-memory addressing: 32-bit shared-window address of the
+// tile plus this lane's (swizzled) chunk offsets, computed once per kernel so
+// every row access in the sweeps is a single LDS/STS.128 at base + r*ROW + off.
 template <typename T, int K>
-__device__ __forceinline__ void load_row(const T* __restrict__ tile, int r, int lane, T (&v)[K]) {
+struct LaneAddr {
   typedef Tile<T, K> L;
-  typedef typename Arith<T>::vec_t V;
-  const T* row = tile + r * L::ROW;
+  uint32_t base;
+  uint32_t off[L::CH];
+  __device__ __forceinline__ LaneAddr(const T* tile, int lane) {
+    base = (uint32_t)__cvta_generic_to_shared(tile);
 #pragma unroll
-  for (int j = 0; j < L::CH; ++j) {
-    const int c = L::swz(lane * L::CH + j);
-    V x = *reinterpret_cast<const V*>(row + c * L::EPC);
-    const T* px = reinterpret_cast<const T*>(&x);
-#pragma unroll
-    for (int q = 0; q < L::EPC; ++q) v[j * L::EPC + q] = px[q];
+    for (int j = 0; j < L::CH; ++j) off[j] = (uint32_t)(L::swz(lane * L::CH + j) * 16);
   }
+  __device__ __forceinline__ uint32_t row(int r) const {
+    return base + (uint32_t)r * (uint32_t)(L::ROW * sizeof(T));
+  }
+};
+
+__device__ __forceinline__ void lds16(uint32_t a, double& x, double& y) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void lds16(uint32_t a, float& x, float& y, float& z, float& w) {
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(x), "=f"(y), "=f"(z), "=f"(w) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void sts16(uint32_t a, double x, double y) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(x), "d"(y) : "memory");
+}
+__device__ __forceinline__ void sts16(uint32_t a, float x, float y, float z, float w) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z),
+               "f"(w) : "memory");
+}
+
+template <int CH>
+__device__ __forceinline__ void load_row_at(uint32_t row, const uint32_t (&off)[CH], double (&v)[2 * CH]) {
+#pragma unroll
+  for (int j = 0; j < CH; ++j) lds16(row + off[j], v[2 * j], v[2 * j + 1]);
+}
+template <int CH>
+__device__ __forceinline__ void load_row_at(uint32_t row, const uint32_t (&off)[CH], float (&v)[4 * CH]) {
+#pragma unroll
+  for (int j = 0; j < CH; ++j) lds16(row + off[j], v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+}
+template <int CH>
+__device__ __forceinline__ void store_row_at(uint32_t row, const uint32_t (&off)[CH], const double (&v)[2 * CH]) {
+#pragma unroll
+  for (int j = 0; j < CH; ++j) sts16(row + off[j], v[2 * j], v[2 * j + 1]);
+}
+template <int CH>
+__device__ __forceinline__ void store_row_at(uint32_t row, const uint32_t (&off)[CH], const float (&v)[4 * CH]) {
+#pragma unroll
+  for (int j = 0; j < CH; ++j) sts16(row + off[j], v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
 }
 
 template <typename T, int K>
-__device__ __forceinline__ void store_row(T* __restrict__ tile, int r, int lane, const T (&v)[K]) {
-  typedef Tile<T, K> L;
-  typedef typename Arith<T>::vec_t V;
-  T* row = tile + r * L::ROW;
-#pragma unroll
-  for (int j = 0; j < L::CH; ++j) {
-    const int c = L::swz(lane * L::CH + j);
-    V x;
-    T* px = reinterpret_cast<T*>(&x);
-#pragma unroll
-    for (int q = 0; q < L::EPC; ++q) px[q] = v[j * L::EPC + q];
-    *reinterpret_cast<V*>(row + c * L::EPC) = x;
-  }
+__device__ __forceinline__ void load_row(const LaneAddr<T, K>& la, int r, T (&v)[K]) {
+  load_row_at<Tile<T, K>::CH>(la.row(r), la.off, v);
+}
+template <typename T, int K>
+__device__ __forceinline__ void store_row(const LaneAddr<T, K>& la, int r, const T (&v)[K]) {
+  store_row_at<Tile<T, K>::CH>(la.row(r), la.off, v);
 }
 
 template <typename T>
@@ -163,89 +195,120 @@ __device__ __forceinline__ void copy_row(const T (&a)[K], T (&b)[K]) {
 // Two-step band sweep. Rows [ya, yb) of the tile receive their t+2 values;
 // 1 <= ya, yb <= Lh-1, yb - ya >= 2. Rows 0 and Lh-1 are the frozen frame.
 // Reads t rows [ya-2, yb+2) ∩ [0, Lh). Foreign rows (outside [ya, yb)) are
-// read before the CTA barrier the caller passes through `bar`; owned rows are
-// written only after it. Every warp of the CTA must call this (idle warps
-// with active=false) because of the barrier inside.
+// read before the CTA barrier inside; owned rows are written only after it.
+// Every warp of the CTA must call this (idle warps with active=false).
+//
+// Software pipeline, one iteration per level-1 row r = ya-1 .. yb+1:
+//   issue  LDS of t(r+2)                 (consumed one iteration later)
+//   L1     b(r)   = stencil(t(r-1), t(r), t(r+1))
+//   L2     out(r-2) = stencil(b(r-3), b(r-2), b(r-1))  -> STS row r-2
+// L1 and L2 of one iteration are independent, doubling the ILP the FP64
+// pipe sees. Rows live in 4-deep rotating register windows (t(q) in slot
+// (q-ya+2)%4, b(q) in slot (q-ya+1)%4) unrolled 4x so every slot is static.
+// Iterations j = r-ya+1 in [3, ...) whose loads hit owned rows run in a
+// branch-free steady loop; the first three and the last few (frozen rows,
+// pre-read halo rows) run through the general iteration.
 // ---------------------------------------------------------------------------
 template <typename T, int K, bool DYN>
-__device__ __forceinline__ void sweep2(T* __restrict__ tile, int Lh, int ya, int yb, bool active,
-                                       const Weights<T>& wt, const LaneCtx& lc) {
-  T a0[K], a1[K], a2[K];   // t rows (rolling)
-  T b0[K], b1[K], b2[K];   // t+1 rows (rolling)
-  T h0[K], h1[K];          // pre-read bottom halo (t rows yb, yb+1)
+__device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya, int yb,
+                                       bool active, const Weights<T>& wt, const LaneCtx& lc) {
+  T t0[K], t1[K], t2[K], t3[K];  // t rows
+  T b0[K], b1[K], b2[K], b3[K];  // t+1 rows
+  T h0[K], h1[K];                // pre-read bottom halo (t rows yb, yb+1)
   T o[K];
   const bool top_frozen = (ya == 1);       // row ya-1 is the frozen frame
   const bool bot_frozen = (yb == Lh - 1);  // row yb is the frozen frame
-  const int lane = lc.lane;
   if (active) {
-    if (!top_frozen) load_row<T, K>(tile, ya - 2, lane, a0);
-    load_row<T, K>(tile, ya - 1, lane, a1);
-    load_row<T, K>(tile, yb, lane, h0);
-    if (!bot_frozen) load_row<T, K>(tile, yb + 1, lane, h1);
+    if (!top_frozen) load_row<T, K>(la, ya - 2, t0);
+    load_row<T, K>(la, ya - 1, t1);
+    load_row<T, K>(la, yb, h0);
+    if (!bot_frozen) load_row<T, K>(la, yb + 1, h1);
   }
   __syncthreads();  // every foreign row is now in registers; owned rows are ours
   if (!active) return;
+  load_row<T, K>(la, ya, t2);
 
-  load_row<T, K>(tile, ya, lane, a2);
-  // level 1, row ya-1
-  if (top_frozen) copy_row<T, K>(a1, b0);
-  else row_update<T, K, DYN>(a0, a1, a2, b0, wt, lc);
-  // level 1, row ya (needs t row ya+1: owned unless the band is 2 rows... yb-ya>=2 so ya+1 < yb)
-  load_row<T, K>(tile, ya + 1, lane, a0);
-  row_update<T, K, DYN>(a1, a2, a0, b1, wt, lc);
-  // window now: t rows ya (a2), ya+1 (a0); t+1 rows ya-1 (b0), ya (b1)
-  // Steady state: for r = ya+1 .. yb: level-1 row r needs t rows r-1,r,r+1;
-  // then level-2 row r-1 from t+1 rows r-2,r-1,r. Unrolled by 3 so the
-  // rolling windows rotate by renaming instead of register moves.
-  int r = ya + 1;
-#define DTB_STEP2(TM1, TC, TP1, BM2, BM1, BR)                                   \
+  // general iteration (any r): sources and frozen rows resolved by branches
+#define DTB_GEN(TM1, TC, TP1, TP2, BR, BM1, BM2, BM3)                            \
   {                                                                              \
-    const int q = r + 1;                                                         \
-    if (q < yb) load_row<T, K>(tile, q, lane, TP1);                              \
-    else if (q == yb) copy_row<T, K>(h0, TP1);                                   \
-    else copy_row<T, K>(h1, TP1);                                                \
-    if (r == yb && bot_frozen) copy_row<T, K>(TC, BR);                           \
-    else row_update<T, K, DYN>(TM1, TC, TP1, BR, wt, lc);                             \
-    row_update<T, K, DYN>(BM2, BM1, BR, o, wt, lc);                                   \
-    store_row<T, K>(tile, r - 1, lane, o);                                       \
+    const int q = r + 2;                                                         \
+    if (q < yb) load_row<T, K>(la, q, TP2);                                      \
+    else if (q == yb) copy_row<T, K>(h0, TP2);                                   \
+    else if (q == yb + 1 && !bot_frozen) copy_row<T, K>(h1, TP2);                \
+    if (r <= yb) {                                                               \
+      if ((r == ya - 1 && top_frozen) || (r == yb && bot_frozen))                \
+        copy_row<T, K>(TC, BR);                                                  \
+      else                                                                       \
+        row_update<T, K, DYN>(TM1, TC, TP1, BR, wt, lc);                         \
+    }                                                                            \
+    if (r >= ya + 2) {                                                           \
+      row_update<T, K, DYN>(BM3, BM2, BM1, o, wt, lc);                           \
+      store_row<T, K>(la, r - 2, o);                                             \
+    }                                                                            \
     ++r;                                                                         \
   }
-  // rotation: (t rows) r-1=a2, r=a0, r+1 -> a1 ; (t+1) r-2=b0, r-1=b1, r -> b2
-  while (r + 2 <= yb) {
-    DTB_STEP2(a2, a0, a1, b0, b1, b2)
-    DTB_STEP2(a0, a1, a2, b1, b2, b0)
-    DTB_STEP2(a1, a2, a0, b2, b0, b1)
+  // steady iteration: r+2 < yb, ya+2 <= r < yb (no frozen row, owned loads)
+#define DTB_STEADY(TM1, TC, TP1, TP2, BR, BM1, BM2, BM3)                         \
+  {                                                                              \
+    load_row_at<Tile<T, K>::CH>(rowp + 2 * kRowBytes, la.off, TP2);              \
+    row_update<T, K, DYN>(TM1, TC, TP1, BR, wt, lc);                             \
+    row_update<T, K, DYN>(BM3, BM2, BM1, o, wt, lc);                             \
+    store_row_at<Tile<T, K>::CH>(rowp - 2 * kRowBytes, la.off, o);               \
+    rowp += kRowBytes;                                                           \
   }
-  if (r <= yb) {
-    DTB_STEP2(a2, a0, a1, b0, b1, b2)
-    if (r <= yb) { DTB_STEP2(a0, a1, a2, b1, b2, b0) }
+  // slot pattern of iteration j (mod 4):
+  //   j%4==0: (t0,t1,t2,t3, b0,b3,b2,b1)   j%4==1: (t1,t2,t3,t0, b1,b0,b3,b2)
+  //   j%4==2: (t2,t3,t0,t1, b2,b1,b0,b3)   j%4==3: (t3,t0,t1,t2, b3,b2,b1,b0)
+  constexpr uint32_t kRowBytes = (uint32_t)(Tile<T, K>::ROW * sizeof(T));
+  int r = ya - 1;
+  DTB_GEN(t0, t1, t2, t3, b0, b3, b2, b1)  // j = 0
+  DTB_GEN(t1, t2, t3, t0, b1, b0, b3, b2)  // j = 1
+  DTB_GEN(t2, t3, t0, t1, b2, b1, b0, b3)  // j = 2
+  // steady blocks of 4 starting at j = 3 (r = ya + 2): need r + 3 + 2 < yb
+  uint32_t rowp = la.row(r);
+  while (r + 5 < yb) {
+    DTB_STEADY(t3, t0, t1, t2, b3, b2, b1, b0)
+    DTB_STEADY(t0, t1, t2, t3, b0, b3, b2, b1)
+    DTB_STEADY(t1, t2, t3, t0, b1, b0, b3, b2)
+    DTB_STEADY(t2, t3, t0, t1, b2, b1, b0, b3)
+    r += 4;
   }
-#undef DTB_STEP2
+  // tail from j = 3 (mod 4) until r > yb + 1
+  while (r <= yb + 1) {
+    DTB_GEN(t3, t0, t1, t2, b3, b2, b1, b0)
+    if (r > yb + 1) break;
+    DTB_GEN(t0, t1, t2, t3, b0, b3, b2, b1)
+    if (r > yb + 1) break;
+    DTB_GEN(t1, t2, t3, t0, b1, b0, b3, b2)
+    if (r > yb + 1) break;
+    DTB_GEN(t2, t3, t0, t1, b2, b1, b0, b3)
+  }
+#undef DTB_GEN
+#undef DTB_STEADY
 }
 
 // One-step band sweep (odd step counts): rows [ya, yb) get t+1;
 // reads t rows [ya-1, yb+1). yb - ya >= 1.
 template <typename T, int K, bool DYN>
-__device__ __forceinline__ void sweep1(T* __restrict__ tile, int Lh, int ya, int yb, bool active,
-                                       const Weights<T>& wt, const LaneCtx& lc) {
+__device__ __forceinline__ void sweep1(const LaneAddr<T, K>& la, int Lh, int ya, int yb,
+                                       bool active, const Weights<T>& wt, const LaneCtx& lc) {
   T a0[K], a1[K], a2[K], h0[K], o[K];
-  const int lane = lc.lane;
   (void)Lh;
   if (active) {
-    load_row<T, K>(tile, ya - 1, lane, a0);
-    load_row<T, K>(tile, yb, lane, h0);
+    load_row<T, K>(la, ya - 1, a0);
+    load_row<T, K>(la, yb, h0);
   }
   __syncthreads();
   if (!active) return;
-  load_row<T, K>(tile, ya, lane, a1);
+  load_row<T, K>(la, ya, a1);
   int r = ya;
 #define DTB_STEP1(TM1, TC, TP1)                                                  \
   {                                                                              \
     const int q = r + 1;                                                         \
-    if (q < yb) load_row<T, K>(tile, q, lane, TP1);                              \
+    if (q < yb) load_row<T, K>(la, q, TP1);                                      \
     else copy_row<T, K>(h0, TP1);                                                \
-    row_update<T, K, DYN>(TM1, TC, TP1, o, wt, lc);                                   \
-    store_row<T, K>(tile, r, lane, o);                                           \
+    row_update<T, K, DYN>(TM1, TC, TP1, o, wt, lc);                              \
+    store_row<T, K>(la, r, o);                                                   \
     ++r;                                                                         \
   }
   while (r + 3 <= yb) {
@@ -277,6 +340,7 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
   const int nw = blockDim.x >> 5;
   LaneCtx lc;
   lc.lane = threadIdx.x & 31;
+  const LaneAddr<T, K> la(tile, lc.lane);
   lc.first = (lc.lane == 0);
   lc.last = (lc.lane == (Lw - 1) / K);
   lc.last_e = (Lw - 1) % K;
@@ -289,7 +353,7 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
     band_rows(Lh, nb2, min(warp, nb2 - 1), ya, yb);
     const bool act = warp < nb2;
     for (; s + 2 <= steps; s += 2) {
-      sweep2<T, K, DYN>(tile, Lh, ya, yb, act, wt, lc);
+      sweep2<T, K, DYN>(la, Lh, ya, yb, act, wt, lc);
       __syncthreads();
     }
   }
@@ -298,7 +362,7 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
     int ya, yb;
     band_rows(Lh, nb1, min(warp, nb1 - 1), ya, yb);
     for (; s < steps; ++s) {
-      sweep1<T, K, DYN>(tile, Lh, ya, yb, warp < nb1, wt, lc);
+      sweep1<T, K, DYN>(la, Lh, ya, yb, warp < nb1, wt, lc);
       __syncthreads();
     }
   }

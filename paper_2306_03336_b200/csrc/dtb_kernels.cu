@@ -32,11 +32,6 @@ namespace dtb {
 
 constexpr int kMaxTiles = 512;  // per dimension
 
-// 32 B of state per lane-row -> 16 warps (<=128 regs); 64 B -> 8 warps (<=255 regs)
-template <typename T, int K>
-struct Shape {
-  static constexpr int kThreads = (K * (int)sizeof(T) <= 32) ? 512 : 256;
-};
 
 // Tile geometry as kernel parameters (<= 32 KB param space on sm_70+ / CUDA 12.1+).
 // col[i] = (owned x0, owned x1, load x0, load x1) in interior coordinates.
@@ -56,37 +51,80 @@ struct Problem {
 };
 
 // ---------------------------------------------------------------------------
-// global <-> smem movement (coalesced along x: one warp per row, lanes stride)
+// global <-> smem movement. A copy is a list of up to 4 tile rectangles
+// flattened into one index space shared by all CTA threads; each thread keeps
+// kBatch independent loads in flight before its stores, so one L2/HBM latency
+// covers the whole copy (the halo refresh is latency-, not bandwidth-bound).
+// Index -> (row, col) uses a 64-bit multiply by a precomputed reciprocal
+// m = ceil(2^32 / width), exact for idx < 2^32 / width.
 // ---------------------------------------------------------------------------
-template <typename T, int K>
-__device__ void load_region(T* tile, const T* __restrict__ g, int64_t pitch, int gx0, int gy0,
-                            int Lw, int Lh, int r0, int r1, int c0, int c1) {
-  // copy tile rows [r0,r1) x cols [c0,c1) from global padded coords (gy0+r, gx0+c)
+template <int N>
+struct RectList {
+  // rect j: rows [r0, r0 + n/w), cols [c0, c0 + w); cells [end[j-1], end[j]) of the
+  // flattened space. set() is called with literal j in order, so after inlining
+  // every array index is static and the struct lives in registers.
+  int r0[N], c0[N], w[N], end[N];
+  uint64_t m[N];
+  __device__ __forceinline__ void set(int j, int ra, int rb, int ca, int cb) {
+    const bool empty = rb <= ra || cb <= ca;
+    r0[j] = ra;
+    c0[j] = ca;
+    w[j] = empty ? 1 : cb - ca;
+    m[j] = (0xFFFFFFFFull + (uint64_t)w[j]) / (uint64_t)w[j];
+    end[j] = (j ? end[j - 1] : 0) + (empty ? 0 : (rb - ra) * (cb - ca));
+  }
+  __device__ __forceinline__ int total() const { return end[N - 1]; }
+  __device__ __forceinline__ void locate(int i, int& r, int& c) const {
+    int rr = r0[0], cc = c0[0], ww = w[0], st = 0;
+    uint64_t mm = m[0];
+#pragma unroll
+    for (int j = 1; j < N; ++j)
+      if (i >= end[j - 1]) { rr = r0[j]; cc = c0[j]; ww = w[j]; mm = m[j]; st = end[j - 1]; }
+    const uint32_t li = (uint32_t)(i - st);
+    const uint32_t q = (uint32_t)(((uint64_t)li * mm) >> 32);
+    r = rr + (int)q;
+    c = cc + (int)(li - q * (uint32_t)ww);
+  }
+};
+
+constexpr int kBatch = 8;
+
+// tile cells of `rl` <- global (padded coords gy0 + r, gx0 + c)
+template <typename T, int K, int N>
+__device__ __forceinline__ void g2s(T* tile, const T* __restrict__ g, int64_t pitch, int gx0,
+                                    int gy0, const RectList<N>& rl) {
   typedef Tile<T, K> L;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  (void)Lw; (void)Lh;
-  for (int r = r0 + warp; r < r1; r += nw) {
-    const T* src = g + (int64_t)(gy0 + r) * pitch + gx0;
-    T* dst = tile + r * L::ROW;
-#pragma unroll 4
-    for (int c = c0 + lane; c < c1; c += 32) {
-      dst[L::swz(c / L::EPC) * L::EPC + (c % L::EPC)] = __ldcg(src + c);
+  const int nt = blockDim.x;
+  for (int base = threadIdx.x; base < rl.total(); base += nt * kBatch) {
+    T v[kBatch];
+    int off[kBatch];
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u) {
+      const int i = base + u * nt;
+      off[u] = -1;
+      if (i < rl.total()) {
+        int r, c;
+        rl.locate(i, r, c);
+        v[u] = __ldcg(g + (int64_t)(gy0 + r) * pitch + (gx0 + c));
+        off[u] = L::at(r, c);
+      }
     }
+#pragma unroll
+    for (int u = 0; u < kBatch; ++u)
+      if (off[u] >= 0) tile[off[u]] = v[u];
   }
 }
 
-template <typename T, int K>
-__device__ void store_region(const T* tile, T* __restrict__ g, int64_t pitch, int gx0, int gy0,
-                             int r0, int r1, int c0, int c1) {
+// global (padded coords) <- tile cells of `rl`
+template <typename T, int K, int N>
+__device__ __forceinline__ void s2g(const T* tile, T* __restrict__ g, int64_t pitch, int gx0,
+                                    int gy0, const RectList<N>& rl) {
   typedef Tile<T, K> L;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int r = r0 + warp; r < r1; r += nw) {
-    T* dst = g + (int64_t)(gy0 + r) * pitch + gx0;
-    const T* src = tile + r * L::ROW;
-#pragma unroll 4
-    for (int c = c0 + lane; c < c1; c += 32) {
-      dst[c] = src[L::swz(c / L::EPC) * L::EPC + (c % L::EPC)];
-    }
+  const int nt = blockDim.x;
+  for (int i = threadIdx.x; i < rl.total(); i += nt) {
+    int r, c;
+    rl.locate(i, r, c);
+    __stcg(g + (int64_t)(gy0 + r) * pitch + (gx0 + c), tile[L::at(r, c)]);
   }
 }
 
@@ -129,8 +167,8 @@ __device__ void advance(T* tile, int Lw, int Lh, int steps, const Weights<T>& wt
 // ---------------------------------------------------------------------------
 // streaming: one pass of h fused steps over every tile
 // ---------------------------------------------------------------------------
-template <typename T, int K, bool DYN>
-__global__ void __launch_bounds__(Shape<T, K>::kThreads, 1)
+template <typename T, int K, int NW, bool DYN>
+__global__ void __launch_bounds__(NW * 32, 1)
 stream_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int nx, int ny,
               Weights<T> wt, int steps, int poison, const __grid_constant__ Geometry geo) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -141,15 +179,22 @@ stream_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int
     const int4 cx = geo.col[tx], cy = geo.row[ty];
     const int Lw = cx.w - cx.z, Lh = cy.w - cy.z;
     // load region in padded coordinates = interior + 1
-    load_region<T, K>(tile, src, pitch, cx.z + 1, cy.z + 1, Lw, Lh, 0, Lh, 0, Lw);
+    {
+      RectList<1> rl;
+      rl.set(0, 0, Lh, 0, Lw);
+      g2s<T, K>(tile, src, pitch, cx.z + 1, cy.z + 1, rl);
+    }
     __syncthreads();
     advance<T, K, DYN>(tile, Lw, Lh, steps, wt, poison != 0, cx.z > -1, cx.w < nx + 1,
                        cy.z > -1, cy.w < ny + 1);
     // owned cells, plus the ghost ring where the tile touches the domain edge
     const int sx0 = cx.x - (cx.x == 0), sx1 = cx.y + (cx.y == nx);
     const int sy0 = cy.x - (cy.x == 0), sy1 = cy.y + (cy.y == ny);
-    store_region<T, K>(tile, dst, pitch, cx.z + 1, cy.z + 1, sy0 - cy.z, sy1 - cy.z, sx0 - cx.z,
-                       sx1 - cx.z);
+    {
+      RectList<1> rl;
+      rl.set(0, sy0 - cy.z, sy1 - cy.z, sx0 - cx.z, sx1 - cx.z);
+      s2g<T, K>(tile, dst, pitch, cx.z + 1, cy.z + 1, rl);
+    }
     __syncthreads();
   }
 }
@@ -166,12 +211,12 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   return v;
 }
 
-template <typename T, int K, bool DYN>
-__global__ void __launch_bounds__(Shape<T, K>::kThreads, 1)
+template <typename T, int K, int NW, bool DYN>
+__global__ void __launch_bounds__(NW * 32, 1)
 resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ xb0,
                 T* __restrict__ xb1, int* __restrict__ flags, int64_t pitch, int nx, int ny,
                 Weights<T> wt, int64_t total_steps, int h, int poison,
-                const __grid_constant__ Geometry geo) {
+                unsigned long long* __restrict__ trace, const __grid_constant__ Geometry geo) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* tile = reinterpret_cast<T*>(smem_raw);
   const int tx = blockIdx.x % geo.ntx, ty = blockIdx.x / geo.ntx;
@@ -180,7 +225,11 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
   const int gx0 = cx.z + 1, gy0 = cy.z + 1;  // padded coords of tile (0,0)
   const bool hl = cx.z > -1, hr = cx.w < nx + 1, ht = cy.z > -1, hb = cy.w < ny + 1;
 
-  load_region<T, K>(tile, in, pitch, gx0, gy0, Lw, Lh, 0, Lh, 0, Lw);
+  {
+    RectList<1> rl;
+    rl.set(0, 0, Lh, 0, Lw);
+    g2s<T, K>(tile, in, pitch, gx0, gy0, rl);
+  }
   __syncthreads();
 
   // how deep each neighbour's load region reaches into my owned cells
@@ -192,26 +241,43 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
   const int ox0 = cx.x - cx.z, ox1 = cx.y - cx.z, oy0 = cy.x - cy.z, oy1 = cy.y - cy.z;
   // halo ring cells to refresh exclude the frozen ghost ring of the domain
   const int rx0 = hl ? 0 : 1, rx1 = hr ? Lw : Lw - 1, ry0 = ht ? 0 : 1, ry1 = hb ? Lh : Lh - 1;
+  RectList<4> band, ring;  // owned cells the neighbours read; halo cells we refresh
+  band.set(0, oy0, oy0 + bt, ox0, ox1);
+  band.set(1, max(oy1 - bb, oy0 + bt), oy1, ox0, ox1);
+  band.set(2, oy0 + bt, oy1 - bb, ox0, ox0 + bl);
+  band.set(3, oy0 + bt, oy1 - bb, max(ox1 - br, ox0 + bl), ox1);
+  ring.set(0, ry0, oy0, rx0, rx1);
+  ring.set(1, oy1, ry1, rx0, rx1);
+  ring.set(2, oy0, oy1, rx0, ox0);
+  ring.set(3, oy0, oy1, ox1, rx1);
 
   int64_t done = 0;
   int epoch = 0;
+  unsigned long long t_comp = 0, t_pub = 0, t_wait = 0, t_ref = 0, tc = 0;
+  const bool tracing = trace != nullptr && threadIdx.x == 0;
+  if (tracing) tc = clock64();
+#define DTB_MARK(acc)                                  \
+  if (tracing) {                                       \
+    const unsigned long long now_ = clock64();         \
+    acc += now_ - tc;                                  \
+    tc = now_;                                         \
+  }
   while (true) {
     const int steps = (int)((total_steps - done) < (int64_t)h ? (total_steps - done) : (int64_t)h);
     advance<T, K, DYN>(tile, Lw, Lh, steps, wt, poison != 0, hl, hr, ht, hb);
     done += steps;
+    DTB_MARK(t_comp)
     if (done >= total_steps) break;
     ++epoch;
     T* xb = (epoch & 1) ? xb1 : xb0;
     // 1. publish the owned band the neighbours' halos cover
-    if (bt) store_region<T, K>(tile, xb, pitch, gx0, gy0, oy0, oy0 + bt, ox0, ox1);
-    if (bb) store_region<T, K>(tile, xb, pitch, gx0, gy0, oy1 - bb, oy1, ox0, ox1);
-    if (bl) store_region<T, K>(tile, xb, pitch, gx0, gy0, oy0, oy1, ox0, ox0 + bl);
-    if (br) store_region<T, K>(tile, xb, pitch, gx0, gy0, oy0, oy1, ox1 - br, ox1);
+    s2g<T, K>(tile, xb, pitch, gx0, gy0, band);
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
       st_release(flags + blockIdx.x, epoch);
     }
+    DTB_MARK(t_pub)
     // 2. wait for the (up to 8) neighbours of this epoch
     if (threadIdx.x < 9 && threadIdx.x != 4) {
       const int dx = (int)threadIdx.x % 3 - 1, dy = (int)threadIdx.x / 3 - 1;
@@ -222,15 +288,22 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
       }
     }
     __syncthreads();
+    DTB_MARK(t_wait)
     // 3. refresh the halo ring (load region minus owned, domain ghost excluded)
-    if (ry0 < oy0) load_region<T, K>(tile, xb, pitch, gx0, gy0, Lw, Lh, ry0, oy0, rx0, rx1);
-    if (oy1 < ry1) load_region<T, K>(tile, xb, pitch, gx0, gy0, Lw, Lh, oy1, ry1, rx0, rx1);
-    if (rx0 < ox0) load_region<T, K>(tile, xb, pitch, gx0, gy0, Lw, Lh, oy0, oy1, rx0, ox0);
-    if (ox1 < rx1) load_region<T, K>(tile, xb, pitch, gx0, gy0, Lw, Lh, oy0, oy1, ox1, rx1);
+    g2s<T, K>(tile, xb, pitch, gx0, gy0, ring);
     __syncthreads();
+    DTB_MARK(t_ref)
   }
-  const int sx0 = ox0 - !hl, sx1 = ox1 + !hr, sy0 = oy0 - !ht, sy1 = oy1 + !hb;
-  store_region<T, K>(tile, out, pitch, gx0, gy0, sy0, sy1, sx0, sx1);
+#undef DTB_MARK
+  if (tracing) {
+    unsigned long long* tr = trace + 5 * blockIdx.x;
+    tr[0] = t_comp; tr[1] = t_pub; tr[2] = t_wait; tr[3] = t_ref; tr[4] = epoch;
+  }
+  {
+    RectList<1> rl;
+    rl.set(0, oy0 - !ht, oy1 + !hb, ox0 - !hl, ox1 + !hr);
+    s2g<T, K>(tile, out, pitch, gx0, gy0, rl);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -287,6 +360,8 @@ using namespace dtb;
 
 thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
+thread_local std::vector<int64_t> g_trace;
+thread_local unsigned g_flags = 0;
 
 int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 int fail(int code, const char* fmt, ...) {
@@ -362,13 +437,12 @@ Weights<T> to_weights(const T w[5]) {
   return k;
 }
 
-template <typename T, int K, bool DYN>
+template <typename T, int K, int NW, bool DYN>
 int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_out,
                         int64_t pitch, int nx, int ny, const Weights<T>& wt,
                         int64_t steps, bool poison, cudaStream_t st) {
-  const int threads = Shape<T, K>::kThreads;
-  if (threads != p.warps * 32)
-    return fail(DTB_EINFEASIBLE, "plan warps %d do not match kernel shape %d", p.warps, threads / 32);
+  const bool tracing = (g_flags & DTB_FLAG_TRACE) != 0;
+  const int threads = NW * 32;
   const int smem = (int)p.smem_bytes;
   const int dev = 0;
   (void)dev;
@@ -376,7 +450,7 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
   int device;
   CUDA_TRY(cudaGetDevice(&device));
   if (p.mode == 0) {
-    auto kern = resident_kernel<T, K, DYN>;
+    auto kern = resident_kernel<T, K, NW, DYN>;
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0;
     CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
@@ -387,28 +461,42 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
                   p.ctas, per_sm * sms);
     void* scratch = nullptr;
     const size_t flag_bytes = 256 + (size_t)p.ctas * sizeof(int);
+    const size_t trace_bytes = (size_t)p.ctas * 5 * sizeof(unsigned long long);
     {
       std::lock_guard<std::mutex> lk(g_mu);
-      int rc = arena_get(g_scratch[device & 15], 2 * grid_bytes + flag_bytes, &scratch);
+      int rc = arena_get(g_scratch[device & 15], 2 * grid_bytes + flag_bytes + trace_bytes + 256,
+                         &scratch);
       if (rc) return rc;
     }
     T* xb0 = reinterpret_cast<T*>(scratch);
     T* xb1 = reinterpret_cast<T*>(reinterpret_cast<char*>(scratch) + grid_bytes);
     int* flags = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + 2 * grid_bytes);
     CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)p.ctas * sizeof(int), st));
+    unsigned long long* trace = nullptr;
+    if (tracing) {
+      trace = reinterpret_cast<unsigned long long*>(
+          reinterpret_cast<char*>(scratch) + ((2 * grid_bytes + flag_bytes + 255) & ~(size_t)255));
+      CUDA_TRY(cudaMemsetAsync(trace, 0, trace_bytes, st));
+    }
     int h = p.h;
     int pois = poison ? 1 : 0;
     void* args[] = {(void*)&d_in, (void*)&d_out, (void*)&xb0, (void*)&xb1, (void*)&flags,
                     (void*)&pitch, (void*)&nx, (void*)&ny, (void*)&wt, (void*)&steps,
-                    (void*)&h, (void*)&pois, (void*)&geo};
+                    (void*)&h, (void*)&pois, (void*)&trace, (void*)&geo};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(p.ctas), dim3(threads), args,
                                          (size_t)smem, st));
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
+    if (tracing) {
+      std::vector<unsigned long long> h_tr((size_t)p.ctas * 5);
+      CUDA_TRY(cudaMemcpyAsync(h_tr.data(), trace, trace_bytes, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      g_trace.assign(h_tr.begin(), h_tr.end());
+    }
     return DTB_OK;
   }
   // streaming passes, ping-ponging dst between out and a scratch grid
-  auto kern = stream_kernel<T, K, DYN>;
+  auto kern = stream_kernel<T, K, NW, DYN>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int64_t passes = (steps + p.h - 1) / p.h;
   T* tmp = nullptr;
@@ -433,22 +521,29 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
   return DTB_OK;
 }
 
+template <typename T, int K, int NW>
+int dispatch_dyn(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch,
+                 int nx, int ny, const Weights<T>& wt, int64_t steps, bool poison,
+                 cudaStream_t st) {
+  return p.dyn() ? launch_plan_kernels<T, K, NW, true>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st)
+                 : launch_plan_kernels<T, K, NW, false>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st);
+}
+
+// kernel shapes compiled (must match the planner's candidates, dtb_plan.cpp)
 template <typename T>
 int dispatch(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch, int nx,
              int ny, const Weights<T>& wt, int64_t steps, bool poison, cudaStream_t st) {
-  const bool dyn = p.dyn();
+#define DTB_SHAPE(KK, WW)                                                                  \
+  if (p.K == KK && p.warps == WW)                                                          \
+    return dispatch_dyn<T, KK, WW>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st);
   if constexpr (sizeof(T) == 8) {
-    if (p.K == 4) return dyn ? launch_plan_kernels<T, 4, true>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st)
-                             : launch_plan_kernels<T, 4, false>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st);
-    if (p.K == 8) return dyn ? launch_plan_kernels<T, 8, true>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st)
-                             : launch_plan_kernels<T, 8, false>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st);
+    DTB_SHAPE(4, 8)
   } else {
-    if (p.K == 8) return dyn ? launch_plan_kernels<T, 8, true>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st)
-                             : launch_plan_kernels<T, 8, false>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st);
-    if (p.K == 16) return dyn ? launch_plan_kernels<T, 16, true>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st)
-                              : launch_plan_kernels<T, 16, false>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st);
+    DTB_SHAPE(8, 8)
   }
-  return fail(DTB_EINFEASIBLE, "no kernel instance for elem %d K %d", (int)sizeof(T), p.K);
+#undef DTB_SHAPE
+  return fail(DTB_EINFEASIBLE, "no kernel instance for elem %d K %d warps %d", (int)sizeof(T),
+              p.K, p.warps);
 }
 
 int validate(int64_t nx, int64_t ny, int64_t pitch, const double w[5], int64_t total_steps,
@@ -514,10 +609,15 @@ int solve_dev(const T* d_in, T* d_out, int64_t nx, int64_t ny, int64_t pitch, co
               cudaStream_t st, dtb_report* rep) {
   double wd[5];
   for (int i = 0; i < 5; ++i) wd[i] = (double)w[i];
-  int rc = validate(nx, ny, pitch, wd, total_steps, t_depth, valid);
+  int rc = validate(nx, ny, pitch, wd, total_steps,
+                    (flags & DTB_FLAG_FORCE_DEPTH) ? 1 : t_depth, valid);
   if (rc) return rc;
+  if ((flags & DTB_FLAG_FORCE_DEPTH) && t_depth < 1)
+    return fail(DTB_EINVAL, "forced depth must be at least 1, got %lld", (long long)t_depth);
   if (d_in == d_out) return fail(DTB_EINVAL, "input and output buffers alias");
   g_launches = 0;
+  g_flags = flags;
+  g_trace.clear();
   // valid-region runs: frozen cells outside `valid` are carried by a plain
   // copy, and the valid rectangle evolves as a standalone problem whose ghost
   // ring is the surrounding frozen cells (engine.py:26-30, grid.py:199-222).
@@ -584,7 +684,8 @@ int solve_host(const T* in, T* out, int64_t nx, int64_t ny, int64_t pitch, const
   if (n_gpus != 1) return fail(DTB_EINVAL, "n_gpus=%d: the host entry point drives one GPU; use the slab API for more", n_gpus);
   double wd[5];
   for (int i = 0; i < 5; ++i) wd[i] = (double)w[i];
-  int rc = validate(nx, ny, pitch, wd, total_steps, t_depth, valid);
+  int rc = validate(nx, ny, pitch, wd, total_steps,
+                    (flags & DTB_FLAG_FORCE_DEPTH) ? 1 : t_depth, valid);
   if (rc) return rc;
   int device;
   CUDA_TRY(cudaGetDevice(&device));
@@ -691,6 +792,12 @@ int dtb_plan(int64_t nx, int64_t ny, int32_t elem_bytes, int64_t total_steps, in
 }
 
 int64_t dtb_last_launch_count(void) { return g_launches; }
+
+int64_t dtb_last_trace(int64_t* out, int64_t n) {
+  const int64_t m = std::min<int64_t>(n, (int64_t)g_trace.size());
+  for (int64_t i = 0; i < m && out; ++i) out[i] = g_trace[(size_t)i];
+  return (int64_t)g_trace.size() / 5;
+}
 
 int dtb_device_info(int32_t* sms, int64_t* smem_optin_per_block, int64_t* l2_bytes,
                     int32_t* cc_major, int32_t* cc_minor) {

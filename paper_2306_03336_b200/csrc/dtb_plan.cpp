@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 namespace dtb {
 
@@ -40,11 +41,11 @@ bool make_split(int N, int n, int h, int align, int maxL, int min_owned, Split& 
     if (ext) {
       // grow the halo into a neighbour (never beyond that neighbour's owned cells)
       int rlim = (i + 1 < n) ? s.o1[i + 1] : N + 1;
-      int take = std::min(ext, rlim - s.l1[i]);
+      int take = std::max(0, std::min(ext, rlim - s.l1[i]));
       s.l1[i] += take;
       ext -= take;
       int llim = (i > 0) ? s.o0[i - 1] : -1;
-      take = std::min(ext, s.l0[i] - llim);
+      take = std::max(0, std::min(ext, s.l0[i] - llim));
       s.l0[i] -= take;
       ext -= take;
       if (ext) s.dyn = true;
@@ -57,6 +58,33 @@ bool make_split(int N, int n, int h, int align, int maxL, int min_owned, Split& 
 namespace {
 
 struct Shape { int K; int warps; };
+
+// kernel shapes compiled into libdtb_b200.so (dtb_kernels.cu dispatch)
+std::vector<Shape> shapes_for(int elem) {
+  std::vector<Shape> v;
+  // 32 B of row state per lane, 8 warps (<= 255 registers: the 4-deep t and
+  // t+1 windows, the pre-read halo rows and the output row stay in registers;
+  // 16 warps (<= 128 registers) and 64 B per lane both spill)
+  if (elem == 8) v = {{4, 8}};
+  else v = {{8, 8}};
+  // DTB_SHAPE=K,W pins one shape (experiments)
+  if (const char* e = getenv("DTB_SHAPE")) {
+    int k = 0, w = 0;
+    if (sscanf(e, "%d,%d", &k, &w) == 2) {
+      std::vector<Shape> f;
+      for (auto& s : v) if (s.K == k && s.warps == w) f.push_back(s);
+      if (!f.empty()) return f;
+    }
+  }
+  return v;
+}
+
+std::vector<int> depths_for(int depth) {
+  std::vector<int> v;
+  if (depth > 0) v.push_back(depth);
+  else for (int h = 2; h <= 32; h += 2) v.push_back(h);
+  return v;
+}
 
 double lanes_per_clk(int elem) { return elem == 8 ? 64.0 : 128.0; }
 // FP32 is issue-bound (FADD/FMUL alone fill the 4 issue slots per SM per
@@ -95,17 +123,13 @@ constexpr double kExchangeLatency = 3500.0;  // flag publish + neighbour poll (~
 bool plan_resident(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& dev,
                    int depth, Plan& best) {
   bool found = false;
-  const Shape shapes8[] = {{4, 16}, {8, 8}};
-  const Shape shapes4[] = {{8, 16}, {16, 8}};
-  const Shape* shapes = elem == 8 ? shapes8 : shapes4;
-  for (int si = 0; si < 2; ++si) {
-    const int K = shapes[si].K, W = shapes[si].warps;
+  for (const Shape& sh : shapes_for(elem)) {
+    const int K = sh.K, W = sh.warps;
     const int Lw_max = 32 * K;
     const int64_t row_bytes = (int64_t)Lw_max * elem;
     const int maxRows = (int)((dev.smem_optin - 1024) / row_bytes);
     if (maxRows < 3) continue;
-    for (int h = 2; h <= 32; h += 2) {
-      if (depth > 0 && h != depth) continue;
+    for (int h : depths_for(depth)) {
       const int hh = (int)std::min<int64_t>(h, std::max<int64_t>(steps, 1));
       const int ntx_min = (int)((nx + 2 + Lw_max - 1) / Lw_max);
       for (int ntx = std::max(1, ntx_min); ntx <= std::min<int64_t>(dev.sms, nx); ++ntx) {
@@ -149,22 +173,21 @@ bool plan_resident(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInf
 bool plan_streaming(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& dev,
                     int depth, Plan& best) {
   bool found = false;
-  const Shape shapes8[] = {{4, 16}, {8, 8}};
-  const Shape shapes4[] = {{8, 16}, {16, 8}};
-  const Shape* shapes = elem == 8 ? shapes8 : shapes4;
-  for (int si = 0; si < 2; ++si) {
-    const int K = shapes[si].K, W = shapes[si].warps;
+  for (const Shape& sh : shapes_for(elem)) {
+    const int K = sh.K, W = sh.warps;
     const int Lw_max = 32 * K;
     const int64_t row_bytes = (int64_t)Lw_max * elem;
     for (int occ = 1; occ <= 2; ++occ) {
       const int64_t smem_cta = std::min<int64_t>(dev.smem_optin, dev.smem_per_sm / occ - 1024);
       const int maxRows = (int)((smem_cta - 1024) / row_bytes);
       if (maxRows < 8) continue;
-      for (int h = 2; h <= 32; h += 2) {
-        if (depth > 0 && h != depth) continue;
+      for (int h : depths_for(depth)) {
         const int hh = (int)std::min<int64_t>(h, std::max<int64_t>(steps, 1));
-        const int ntx_min = (int)((nx + 2 + Lw_max - 1) / Lw_max);
-        for (int ntx = std::max(1, ntx_min); ntx <= ntx_min + 2 && ntx <= nx; ++ntx) {
+        // interior tiles own at most Lw_max - 2h columns
+        const int per = std::max(1, Lw_max - 2 * h);
+        const int ntx_min = (int)std::max<int64_t>(1, std::max<int64_t>(
+            (nx + 2 + Lw_max - 1) / Lw_max, (nx + per - 1) / per - 1));
+        for (int ntx = ntx_min; ntx <= ntx_min + 3 && ntx <= nx; ++ntx) {
           Split sx;
           if (!make_split((int)nx, ntx, h, K, Lw_max, 1, sx)) continue;
           // tallest tiles that fit
