@@ -12,7 +12,7 @@ import os
 from ctypes import POINTER, c_char_p, c_double, c_float, c_int, c_int32, c_int64, c_uint, c_uint64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdtb_b200.so")
+LIB_PATH = os.environ.get("DTB_LIB") or os.path.join(_HERE, "libdtb_b200.so")  # DTB_LIB: A/B builds
 
 DTB_OK = 0
 DTB_EINVAL = 1

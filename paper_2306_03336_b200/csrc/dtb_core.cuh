@@ -35,6 +35,21 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Schedule variants (compile-time, for A/B measurement; defaults are the product)
+#ifndef DTB_ROW2
+#define DTB_ROW2 0      // steady loop evaluates L1/L2 rows stage-major together
+#endif
+#ifndef DTB_FASTPATH
+#define DTB_FASTPATH 1  // static sweep schedule for bands of 4k rows
+#endif
+#ifndef DTB_PUBREG
+#define DTB_PUBREG 0    // resident publish: 0 smem pass after the epoch, 1 from registers
+                        // inside the last sweep, 2 each warp right after its own last sweep
+#endif
+#ifndef DTB_RING
+#define DTB_RING 1      // resident: specialised cp.async halo refresh
+#endif
+
 namespace dtb {
 
 template <typename T> struct Arith;
@@ -185,11 +200,115 @@ __device__ __forceinline__ void row_update(const T (&up)[K], const T (&mid)[K], 
   }
 }
 
+// Two independent row updates evaluated stage-major: every accumulation
+// stage (w, e, s, c, n) is issued for all 2K cells before the next, so the
+// FP pipe always has 2K independent dependency chains in flight (the
+// accumulation order within each cell is still W,E,S,C,N — only the
+// interleaving across cells changes, which cannot change any result).
+template <typename T, int K, bool DYN>
+__device__ __forceinline__ void row_update2(const T (&ua)[K], const T (&ma)[K], const T (&da)[K],
+                                            T (&oa)[K], const T (&ub)[K], const T (&mb)[K],
+                                            const T (&db)[K], T (&ob)[K], const Weights<T>& wt,
+                                            const LaneCtx& lc) {
+  typedef Arith<T> A;
+  const T wa = shfl_up1(ma[K - 1]), ea = shfl_dn1(ma[0]);
+  const T wb = shfl_up1(mb[K - 1]), eb = shfl_dn1(mb[0]);
+#pragma unroll
+  for (int e = 0; e < K; ++e) {
+    oa[e] = A::mul((e == 0) ? wa : ma[e - 1], wt.w);
+    ob[e] = A::mul((e == 0) ? wb : mb[e - 1], wt.w);
+  }
+#pragma unroll
+  for (int e = 0; e < K; ++e) {
+    oa[e] = A::add(oa[e], A::mul((e == K - 1) ? ea : ma[e + 1], wt.e));
+    ob[e] = A::add(ob[e], A::mul((e == K - 1) ? eb : mb[e + 1], wt.e));
+  }
+#pragma unroll
+  for (int e = 0; e < K; ++e) {
+    oa[e] = A::add(oa[e], A::mul(ua[e], wt.s));
+    ob[e] = A::add(ob[e], A::mul(ub[e], wt.s));
+  }
+#pragma unroll
+  for (int e = 0; e < K; ++e) {
+    oa[e] = A::add(oa[e], A::mul(ma[e], wt.c));
+    ob[e] = A::add(ob[e], A::mul(mb[e], wt.c));
+  }
+#pragma unroll
+  for (int e = 0; e < K; ++e) {
+    oa[e] = A::add(oa[e], A::mul(da[e], wt.n));
+    ob[e] = A::add(ob[e], A::mul(db[e], wt.n));
+  }
+  if (lc.first) { oa[0] = ma[0]; ob[0] = mb[0]; }
+  if (DYN) {
+    if (lc.last) {
+#pragma unroll
+      for (int e = 0; e < K; ++e)
+        if (e == lc.last_e) { oa[e] = ma[e]; ob[e] = mb[e]; }
+    }
+  } else {
+    if (lc.last) { oa[K - 1] = ma[K - 1]; ob[K - 1] = mb[K - 1]; }
+  }
+}
+
 template <typename T, int K>
 __device__ __forceinline__ void copy_row(const T (&a)[K], T (&b)[K]) {
 #pragma unroll
   for (int e = 0; e < K; ++e) b[e] = a[e];
 }
+
+// Publisher: during the last sweep of a resident epoch, every freshly
+// computed row that lies in the CTA's owned band (the cells its neighbours'
+// halos cover) is also stored straight from registers to the L2 exchange
+// buffer — the halo publish costs a few predicated STGs instead of a pass
+// over shared memory. Rows [top0, top1) and [bot0, bot1) publish every owned
+// column (full_mask); other owned rows [own0, own1) only the side columns.
+__device__ __forceinline__ void st_pred(bool p, double* a, double v) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %0, 0; @q st.global.cg.f64 [%1], %2; }"
+               ::"r"((unsigned)p), "l"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_pred(bool p, float* a, float v) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %0, 0; @q st.global.cg.f32 [%1], %2; }"
+               ::"r"((unsigned)p), "l"(a), "f"(v) : "memory");
+}
+
+// Publisher: during the last sweep of a resident epoch, rows of the owned
+// top/bottom band (the rows the y-neighbours' halos cover, [own0, top1) and
+// [bot0, own1)) are also stored straight from registers to the L2 exchange
+// buffer (K predicated stores per lane, no branch). Only the warps whose band
+// contains such rows run the publishing variant of the sweep; the narrow
+// side columns are published from smem after the sweep.
+template <typename T, int K>
+struct Publisher {
+  T* g;             // exchange buffer at (tile row 0, this lane's first column)
+  int64_t pitch;
+  int own0, own1, top1, bot0;
+  uint32_t full_mask, side_mask;
+  // mode 2: publish the band's own rows [ya, yb) from smem (they are final once
+  // the band's last sweep is done: no other warp writes them)
+  __device__ __forceinline__ void put_band(const LaneAddr<T, K>& la, int ya, int yb) const {
+    const int r0 = max(ya, own0), r1 = min(yb, own1);
+    for (int row = r0; row < r1; ++row) {
+      const uint32_t m = (row < top1 || row >= bot0) ? full_mask : side_mask;
+      if (__any_sync(0xffffffffu, m != 0u)) {
+        T v[K];
+        load_row<T, K>(la, row, v);
+        T* p = g + (int64_t)row * pitch;
+#pragma unroll
+        for (int e = 0; e < K; ++e) st_pred(((m >> e) & 1u) != 0, p + e, v[e]);
+      }
+    }
+  }
+  __device__ __forceinline__ bool covers(int ya, int yb) const {
+    return (ya < top1 && yb > own0) || (ya < own1 && yb > bot0);
+  }
+  __device__ __forceinline__ void put(int row, const T (&v)[K]) const {
+    const bool in = (row >= own0 && row < top1) || (row >= bot0 && row < own1);
+    const uint32_t m = in ? full_mask : 0u;
+    T* p = g + (int64_t)row * pitch;
+#pragma unroll
+    for (int e = 0; e < K; ++e) st_pred(((m >> e) & 1u) != 0, p + e, v[e]);
+  }
+};
 
 // ---------------------------------------------------------------------------
 // Two-step band sweep. Rows [ya, yb) of the tile receive their t+2 values;
@@ -209,9 +328,10 @@ __device__ __forceinline__ void copy_row(const T (&a)[K], T (&b)[K]) {
 // branch-free steady loop; the first three and the last few (frozen rows,
 // pre-read halo rows) run through the general iteration.
 // ---------------------------------------------------------------------------
-template <typename T, int K, bool DYN>
+template <typename T, int K, bool DYN, bool PUB>
 __device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya, int yb,
-                                       bool active, const Weights<T>& wt, const LaneCtx& lc) {
+                                       bool active, const Weights<T>& wt, const LaneCtx& lc,
+                                       const Publisher<T, K>& pub) {
   T t0[K], t1[K], t2[K], t3[K];  // t rows
   T b0[K], b1[K], b2[K], b3[K];  // t+1 rows
   T h0[K], h1[K];                // pre-read bottom halo (t rows yb, yb+1)
@@ -228,6 +348,67 @@ __device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya,
   if (!active) return;
   load_row<T, K>(la, ya, t2);
 
+  constexpr uint32_t kRowBytes = (uint32_t)(Tile<T, K>::ROW * sizeof(T));
+  // steady iteration: r+2 < yb, ya+2 <= r < yb (no frozen row, owned loads)
+#define DTB_STEADY(TM1, TC, TP1, TP2, BR, BM1, BM2, BM3)                         \
+  {                                                                              \
+    load_row_at<Tile<T, K>::CH>(rowp + 2 * kRowBytes, la.off, TP2);              \
+    if (DTB_ROW2) {                                                              \
+      row_update2<T, K, DYN>(TM1, TC, TP1, BR, BM3, BM2, BM1, o, wt, lc);        \
+    } else {                                                                     \
+      row_update<T, K, DYN>(TM1, TC, TP1, BR, wt, lc);                           \
+      row_update<T, K, DYN>(BM3, BM2, BM1, o, wt, lc);                           \
+    }                                                                            \
+    store_row_at<Tile<T, K>::CH>(rowp - 2 * kRowBytes, la.off, o);               \
+    if (PUB) pub.put(rr - 2, o);                                                 \
+    rowp += kRowBytes;                                                           \
+    ++rr;                                                                        \
+  }
+  const int H = yb - ya;
+  if (DTB_FASTPATH && (H & 3) == 0 && H >= 4) {
+    // ---- fast path: band height a multiple of 4 -> fully static schedule ----
+    // j=0 (r=ya-1): L1(ya-1); load t(ya+1)
+    load_row<T, K>(la, ya + 1, t3);
+    if (top_frozen) copy_row<T, K>(t1, b0);
+    else row_update<T, K, DYN>(t0, t1, t2, b0, wt, lc);
+    // j=1 (r=ya): L1(ya); load t(ya+2)
+    load_row<T, K>(la, ya + 2, t0);
+    row_update<T, K, DYN>(t1, t2, t3, b1, wt, lc);
+    // j=2 (r=ya+1): L1(ya+1); load t(ya+3)
+    load_row<T, K>(la, ya + 3, t1);
+    row_update<T, K, DYN>(t2, t3, t0, b2, wt, lc);
+    // steady j=3 .. H-2 (r = ya+2 .. yb-3), (H-4)/4 blocks
+    uint32_t rowp = la.row(ya + 2);
+    int rr = ya + 2;
+    for (int blk = (H - 4) >> 2; blk > 0; --blk) {
+      DTB_STEADY(t3, t0, t1, t2, b3, b2, b1, b0)
+      DTB_STEADY(t0, t1, t2, t3, b0, b3, b2, b1)
+      DTB_STEADY(t1, t2, t3, t0, b1, b0, b3, b2)
+      DTB_STEADY(t2, t3, t0, t1, b2, b1, b0, b3)
+    }
+    // tail j=H-1 (r=yb-2): t(yb) is h0; L1(yb-2), L2(yb-4)
+    row_update2<T, K, DYN>(t3, t0, t1, b3, b0, b1, b2, o, wt, lc);
+    store_row<T, K>(la, yb - 4, o);
+    if (PUB) pub.put(yb - 4, o);
+    // r=yb-1: L1(yb-1) from (t0, t1, h0), L2(yb-3) from (b1, b2, b3)
+    row_update2<T, K, DYN>(t0, t1, h0, b0, b1, b2, b3, o, wt, lc);
+    store_row<T, K>(la, yb - 3, o);
+    if (PUB) pub.put(yb - 3, o);
+    // r=yb: L1(yb) (frozen row, or from (t1, h0, h1)), L2(yb-2) from (b2, b3, b0)
+    if (bot_frozen) {
+      copy_row<T, K>(h0, b1);
+      row_update<T, K, DYN>(b2, b3, b0, o, wt, lc);
+    } else {
+      row_update2<T, K, DYN>(t1, h0, h1, b1, b2, b3, b0, o, wt, lc);
+    }
+    store_row<T, K>(la, yb - 2, o);
+    if (PUB) pub.put(yb - 2, o);
+    // r=yb+1: L2(yb-1) from (b3, b0, b1)
+    row_update<T, K, DYN>(b3, b0, b1, o, wt, lc);
+    store_row<T, K>(la, yb - 1, o);
+    if (PUB) pub.put(yb - 1, o);
+    return;
+  }
   // general iteration (any r): sources and frozen rows resolved by branches
 #define DTB_GEN(TM1, TC, TP1, TP2, BR, BM1, BM2, BM3)                            \
   {                                                                              \
@@ -244,22 +425,14 @@ __device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya,
     if (r >= ya + 2) {                                                           \
       row_update<T, K, DYN>(BM3, BM2, BM1, o, wt, lc);                           \
       store_row<T, K>(la, r - 2, o);                                             \
+      if (PUB) pub.put(r - 2, o);                                                \
     }                                                                            \
     ++r;                                                                         \
-  }
-  // steady iteration: r+2 < yb, ya+2 <= r < yb (no frozen row, owned loads)
-#define DTB_STEADY(TM1, TC, TP1, TP2, BR, BM1, BM2, BM3)                         \
-  {                                                                              \
-    load_row_at<Tile<T, K>::CH>(rowp + 2 * kRowBytes, la.off, TP2);              \
-    row_update<T, K, DYN>(TM1, TC, TP1, BR, wt, lc);                             \
-    row_update<T, K, DYN>(BM3, BM2, BM1, o, wt, lc);                             \
-    store_row_at<Tile<T, K>::CH>(rowp - 2 * kRowBytes, la.off, o);               \
-    rowp += kRowBytes;                                                           \
   }
   // slot pattern of iteration j (mod 4):
   //   j%4==0: (t0,t1,t2,t3, b0,b3,b2,b1)   j%4==1: (t1,t2,t3,t0, b1,b0,b3,b2)
   //   j%4==2: (t2,t3,t0,t1, b2,b1,b0,b3)   j%4==3: (t3,t0,t1,t2, b3,b2,b1,b0)
-  constexpr uint32_t kRowBytes = (uint32_t)(Tile<T, K>::ROW * sizeof(T));
+  // ---- general path (any band height >= 2) ----
   int r = ya - 1;
   DTB_GEN(t0, t1, t2, t3, b0, b3, b2, b1)  // j = 0
   DTB_GEN(t1, t2, t3, t0, b1, b0, b3, b2)  // j = 1
@@ -267,6 +440,7 @@ __device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya,
   // steady blocks of 4 starting at j = 3 (r = ya + 2): need r + 3 + 2 < yb
   uint32_t rowp = la.row(r);
   while (r + 5 < yb) {
+    int rr = r;
     DTB_STEADY(t3, t0, t1, t2, b3, b2, b1, b0)
     DTB_STEADY(t0, t1, t2, t3, b0, b3, b2, b1)
     DTB_STEADY(t1, t2, t3, t0, b1, b0, b3, b2)
@@ -289,9 +463,10 @@ __device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya,
 
 // One-step band sweep (odd step counts): rows [ya, yb) get t+1;
 // reads t rows [ya-1, yb+1). yb - ya >= 1.
-template <typename T, int K, bool DYN>
+template <typename T, int K, bool DYN, bool PUB>
 __device__ __forceinline__ void sweep1(const LaneAddr<T, K>& la, int Lh, int ya, int yb,
-                                       bool active, const Weights<T>& wt, const LaneCtx& lc) {
+                                       bool active, const Weights<T>& wt, const LaneCtx& lc,
+                                       const Publisher<T, K>& pub) {
   T a0[K], a1[K], a2[K], h0[K], o[K];
   (void)Lh;
   if (active) {
@@ -309,6 +484,7 @@ __device__ __forceinline__ void sweep1(const LaneAddr<T, K>& la, int Lh, int ya,
     else copy_row<T, K>(h0, TP1);                                                \
     row_update<T, K, DYN>(TM1, TC, TP1, o, wt, lc);                              \
     store_row<T, K>(la, r, o);                                                   \
+    if (PUB) pub.put(r, o);                                                      \
     ++r;                                                                         \
   }
   while (r + 3 <= yb) {
@@ -332,10 +508,26 @@ __device__ __forceinline__ void band_rows(int Lh, int nb, int b, int& ya, int& y
   yb = ya + base + (b < rem ? 1 : 0);
 }
 
+// Two-step sweeps: band heights in whole multiples of 4 where possible (the
+// static fast path of sweep2); the remainder rows go to the last band.
+__device__ __forceinline__ void band_rows4(int Lh, int nb, int b, int& ya, int& yb) {
+  const int rows = Lh - 2;
+  const int q = rows >> 2;  // whole 4-row quads
+  if (q < nb) {
+    band_rows(Lh, nb, b, ya, yb);
+    return;
+  }
+  const int base = q / nb, rem = q % nb;
+  ya = 1 + 4 * (b * base + min(b, rem));
+  yb = ya + 4 * (base + (b < rem ? 1 : 0));
+  if (b == nb - 1) yb = Lh - 1;
+}
+
 // Advance the tile `steps` time steps in place. All threads of the CTA call.
+// With `pub` non-null the final sweep also publishes the owned band.
 template <typename T, int K, bool DYN>
 __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
-                             const Weights<T>& wt) {
+                             const Weights<T>& wt, const Publisher<T, K>* pub = nullptr) {
   const int warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
   LaneCtx lc;
@@ -346,14 +538,22 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
   lc.last_e = (Lw - 1) % K;
   const int rows = Lh - 2;
   if (rows <= 0 || Lw <= 2) return;
+  Publisher<T, K> nopub;
+  const Publisher<T, K>& pb = pub ? *pub : nopub;
   int s = 0;
   if (steps >= 2 && rows >= 2) {
     const int nb2 = max(1, min(nw, rows / 2));
     int ya, yb;
-    band_rows(Lh, nb2, min(warp, nb2 - 1), ya, yb);
+    band_rows4(Lh, nb2, min(warp, nb2 - 1), ya, yb);
     const bool act = warp < nb2;
+    const bool band_pub = DTB_PUBREG == 1 && pub && pub->covers(ya, yb);
     for (; s + 2 <= steps; s += 2) {
-      sweep2<T, K, DYN>(la, Lh, ya, yb, act, wt, lc);
+      if (band_pub && s + 2 == steps) sweep2<T, K, DYN, true>(la, Lh, ya, yb, act, wt, lc, pb);
+      else sweep2<T, K, DYN, false>(la, Lh, ya, yb, act, wt, lc, pb);
+      if (DTB_PUBREG == 2 && pub && act && s + 2 == steps) {
+        pub->put_band(la, ya, yb);  // this warp's rows are final: publish them now
+        __threadfence();
+      }
       __syncthreads();
     }
   }
@@ -361,8 +561,14 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
     const int nb1 = max(1, min(nw, rows));
     int ya, yb;
     band_rows(Lh, nb1, min(warp, nb1 - 1), ya, yb);
+    const bool band_pub = DTB_PUBREG == 1 && pub && pub->covers(ya, yb);
     for (; s < steps; ++s) {
-      sweep1<T, K, DYN>(la, Lh, ya, yb, warp < nb1, wt, lc);
+      if (band_pub && s + 1 == steps) sweep1<T, K, DYN, true>(la, Lh, ya, yb, warp < nb1, wt, lc, pb);
+      else sweep1<T, K, DYN, false>(la, Lh, ya, yb, warp < nb1, wt, lc, pb);
+      if (DTB_PUBREG == 2 && pub && warp < nb1 && s + 1 == steps) {
+        pub->put_band(la, ya, yb);
+        __threadfence();
+      }
       __syncthreads();
     }
   }

@@ -52,11 +52,8 @@ struct Problem {
 
 // ---------------------------------------------------------------------------
 // global <-> smem movement. A copy is a list of up to 4 tile rectangles
-// flattened into one index space shared by all CTA threads; each thread keeps
-// kBatch independent loads in flight before its stores, so one L2/HBM latency
-// covers the whole copy (the halo refresh is latency-, not bandwidth-bound).
-// Index -> (row, col) uses a 64-bit multiply by a precomputed reciprocal
-// m = ceil(2^32 / width), exact for idx < 2^32 / width.
+// spread over all CTA threads. Index -> (row, col) uses a 64-bit multiply by
+// a precomputed reciprocal m = ceil(2^32 / width), exact for idx < 2^32/width.
 // ---------------------------------------------------------------------------
 template <int N>
 struct RectList {
@@ -87,32 +84,40 @@ struct RectList {
   }
 };
 
-constexpr int kBatch = 8;
 
-// tile cells of `rl` <- global (padded coords gy0 + r, gx0 + c)
+__device__ __forceinline__ void cp_async(uint32_t dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async(uint32_t dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// tile cells of `rl` <- global (padded coords gy0 + r, gx0 + c), as
+// asynchronous global->shared copies (LDGSTS): no registers are held, every
+// copy of the CTA is in flight at once, one L2/HBM latency covers the lot.
+// The caller must __syncthreads() afterwards.
 template <typename T, int K, int N>
 __device__ __forceinline__ void g2s(T* tile, const T* __restrict__ g, int64_t pitch, int gx0,
                                     int gy0, const RectList<N>& rl) {
   typedef Tile<T, K> L;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
   const int nt = blockDim.x;
-  for (int base = threadIdx.x; base < rl.total(); base += nt * kBatch) {
-    T v[kBatch];
-    int off[kBatch];
 #pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-      const int i = base + u * nt;
-      off[u] = -1;
-      if (i < rl.total()) {
-        int r, c;
-        rl.locate(i, r, c);
-        v[u] = __ldcg(g + (int64_t)(gy0 + r) * pitch + (gx0 + c));
-        off[u] = L::at(r, c);
-      }
+  for (int j = 0; j < N; ++j) {
+    const int n = rl.end[j] - (j ? rl.end[j - 1] : 0);
+    const uint32_t w = (uint32_t)rl.w[j];
+    const uint64_t m = rl.m[j];
+    for (int i = threadIdx.x; i < n; i += nt) {
+      const uint32_t q = (uint32_t)(((uint64_t)(uint32_t)i * m) >> 32);
+      const int r = rl.r0[j] + (int)q, c = rl.c0[j] + (int)((uint32_t)i - q * w);
+      cp_async(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)),
+               g + (int64_t)(gy0 + r) * pitch + (gx0 + c));
     }
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u)
-      if (off[u] >= 0) tile[off[u]] = v[u];
   }
+  cp_async_wait_all();
 }
 
 // global (padded coords) <- tile cells of `rl`
@@ -125,6 +130,82 @@ __device__ __forceinline__ void s2g(const T* tile, T* __restrict__ g, int64_t pi
     int r, c;
     rl.locate(i, r, c);
     __stcg(g + (int64_t)(gy0 + r) * pitch + (gx0 + c), tile[L::at(r, c)]);
+  }
+}
+
+// Resident halo refresh: top/bottom ring rows one warp per row (coalesced),
+// side ring columns one thread per row; all as cp.async, one latency.
+template <typename T, int K>
+__device__ __forceinline__ void refresh_ring(T* tile, const T* __restrict__ g, int64_t pitch,
+                                             int gx0, int gy0, int ry0, int oy0, int oy1, int ry1,
+                                             int rx0, int ox0, int ox1, int rx1) {
+  typedef Tile<T, K> L;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int ntop = oy0 - ry0, nrows = ntop + (ry1 - oy1);
+  for (int k = warp; k < nrows; k += nw) {
+    const int r = k < ntop ? ry0 + k : oy1 + (k - ntop);
+    const T* src = g + (int64_t)(gy0 + r) * pitch + gx0;
+    for (int c = rx0 + lane; c < rx1; c += 32)
+      cp_async(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)), src + c);
+  }
+  for (int r = oy0 + threadIdx.x; r < oy1; r += blockDim.x) {
+    const T* src = g + (int64_t)(gy0 + r) * pitch + gx0;
+    for (int c = rx0; c < ox0; ++c) cp_async(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)), src + c);
+    for (int c = ox1; c < rx1; ++c) cp_async(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)), src + c);
+  }
+  cp_async_wait_all();
+}
+
+__device__ __forceinline__ double lds_elem(uint32_t a, double) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float lds_elem(uint32_t a, float) {
+  float v;
+  asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+
+// Resident publish of the owned band: rows [oy0, t1) and [b0, oy1) in full
+// (one warp per row, coalesced), and the side columns [ox0, c1), [c2, ox1) of
+// the rows in between (one thread per row).
+template <typename T, int K>
+__device__ __forceinline__ void publish_band(const T* tile, T* __restrict__ g, int64_t pitch,
+                                             int gx0, int gy0, int oy0, int t1, int b0, int oy1,
+                                             int ox0, int c1, int c2, int ox1) {
+  typedef Tile<T, K> L;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int ntop = t1 - oy0, nrows = ntop + (oy1 - b0);
+  for (int k = warp; k < nrows; k += nw) {
+    const int r = k < ntop ? oy0 + k : b0 + (k - ntop);
+    T* dst = g + (int64_t)(gy0 + r) * pitch + gx0;
+#pragma unroll 4
+    for (int c = ox0 + lane; c < ox1; c += 32)
+      dst[c] = lds_elem(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)), T());
+  }
+  for (int r = t1 + threadIdx.x; r < b0; r += blockDim.x) {
+    T* dst = g + (int64_t)(gy0 + r) * pitch + gx0;
+    for (int c = ox0; c < c1; ++c)
+      dst[c] = lds_elem(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)), T());
+    for (int c = c2; c < ox1; ++c)
+      dst[c] = lds_elem(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)), T());
+  }
+}
+
+// Resident publish of the side columns [c0, c1) and [c2, c3) of rows [r0, r1):
+// one thread per row.
+template <typename T, int K>
+__device__ __forceinline__ void publish_sides(const T* tile, T* __restrict__ g, int64_t pitch,
+                                              int gx0, int gy0, int r0, int r1, int c0, int c1,
+                                              int c2, int c3) {
+  typedef Tile<T, K> L;
+  for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    T* dst = g + (int64_t)(gy0 + r) * pitch + gx0;
+    for (int c = c0; c < c1; ++c) __stcg(dst + c, tile[L::at(r, c)]);
+    for (int c = c2; c < c3; ++c) __stcg(dst + c, tile[L::at(r, c)]);
   }
 }
 
@@ -151,9 +232,10 @@ __device__ void poison_rim(T* tile, int Lw, int Lh, int done, bool hl, bool hr, 
 
 template <typename T, int K, bool DYN>
 __device__ void advance(T* tile, int Lw, int Lh, int steps, const Weights<T>& wt, bool poison,
-                        bool hl, bool hr, bool ht, bool hb) {
+                        bool hl, bool hr, bool ht, bool hb,
+                        const Publisher<T, K>* pub = nullptr) {
   if (!poison) {
-    advance_tile<T, K, DYN>(tile, Lw, Lh, steps, wt);
+    advance_tile<T, K, DYN>(tile, Lw, Lh, steps, wt, pub);
     return;
   }
   // poison mode: one step at a time, NaN the stale rim after each
@@ -210,6 +292,11 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 template <typename T, int K, int NW, bool DYN>
 __global__ void __launch_bounds__(NW * 32, 1)
@@ -241,15 +328,6 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
   const int ox0 = cx.x - cx.z, ox1 = cx.y - cx.z, oy0 = cy.x - cy.z, oy1 = cy.y - cy.z;
   // halo ring cells to refresh exclude the frozen ghost ring of the domain
   const int rx0 = hl ? 0 : 1, rx1 = hr ? Lw : Lw - 1, ry0 = ht ? 0 : 1, ry1 = hb ? Lh : Lh - 1;
-  RectList<4> band, ring;  // owned cells the neighbours read; halo cells we refresh
-  band.set(0, oy0, oy0 + bt, ox0, ox1);
-  band.set(1, max(oy1 - bb, oy0 + bt), oy1, ox0, ox1);
-  band.set(2, oy0 + bt, oy1 - bb, ox0, ox0 + bl);
-  band.set(3, oy0 + bt, oy1 - bb, max(ox1 - br, ox0 + bl), ox1);
-  ring.set(0, ry0, oy0, rx0, rx1);
-  ring.set(1, oy1, ry1, rx0, rx1);
-  ring.set(2, oy0, oy1, rx0, ox0);
-  ring.set(3, oy0, oy1, ox1, rx1);
 
   int64_t done = 0;
   int epoch = 0;
@@ -262,20 +340,64 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     acc += now_ - tc;                                  \
     tc = now_;                                         \
   }
+  // per-lane publish masks over the lane's K columns (tile coordinates)
+  Publisher<T, K> pub;
+  pub.pitch = pitch;
+  pub.own0 = oy0;
+  pub.own1 = oy1;
+  pub.top1 = oy0 + bt;
+  pub.bot0 = oy1 - bb;
+  pub.full_mask = 0;
+  pub.side_mask = 0;
+  {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int e = 0; e < K; ++e) {
+      const int c = lane * K + e;
+      if (c >= ox0 && c < ox1) {
+        pub.full_mask |= 1u << e;
+        if (c < ox0 + bl || c >= ox1 - br) pub.side_mask |= 1u << e;
+      }
+    }
+  }
   while (true) {
     const int steps = (int)((total_steps - done) < (int64_t)h ? (total_steps - done) : (int64_t)h);
-    advance<T, K, DYN>(tile, Lw, Lh, steps, wt, poison != 0, hl, hr, ht, hb);
+    const bool last = done + steps >= total_steps;
+    T* xb = ((epoch + 1) & 1) ? xb1 : xb0;
+    pub.g = xb + (int64_t)gy0 * pitch + gx0 + (threadIdx.x & 31) * K;
+    // 1. compute the epoch; its final sweep publishes the owned band from registers
+    advance<T, K, DYN>(tile, Lw, Lh, steps, wt, poison != 0, hl, hr, ht, hb,
+                       (last || poison || !DTB_PUBREG) ? nullptr : &pub);
     done += steps;
     DTB_MARK(t_comp)
-    if (done >= total_steps) break;
+    if (last) break;
     ++epoch;
-    T* xb = (epoch & 1) ? xb1 : xb0;
-    // 1. publish the owned band the neighbours' halos cover
-    s2g<T, K>(tile, xb, pitch, gx0, gy0, band);
+    if (!poison && DTB_PUBREG == 0) {
+      const int t1 = min(oy0 + bt, oy1), b0 = max(oy1 - bb, t1);
+      publish_band<T, K>(tile, xb, pitch, gx0, gy0, oy0, t1, b0, oy1, ox0, ox0 + bl,
+                         max(ox1 - br, ox0 + bl), ox1);
+    } else if (poison) {
+      // poison mode publishes through smem (its sweeps run one step at a time)
+      RectList<4> band;  // owned cells the neighbours' halos cover
+      band.set(0, oy0, oy0 + bt, ox0, ox1);
+      band.set(1, max(oy1 - bb, oy0 + bt), oy1, ox0, ox1);
+      band.set(2, oy0 + bt, oy1 - bb, ox0, ox0 + bl);
+      band.set(3, oy0 + bt, oy1 - bb, max(ox1 - br, ox0 + bl), ox1);
+      s2g<T, K>(tile, xb, pitch, gx0, gy0, band);
+    } else if (DTB_PUBREG == 1) {
+      // side columns of the owned rows between the top/bottom bands
+      publish_sides<T, K>(tile, xb, pitch, gx0, gy0, oy0 + bt, oy1 - bb, ox0, ox0 + bl,
+                          max(ox1 - br, ox0 + bl), ox1);
+    }
+#ifndef DTB_FENCE
+#define DTB_FENCE 0  // 0: thread 0 st.release after the barrier; 1: every thread fences first;
+                     // 9: no fence (timing experiments only - unsynchronised)
+#endif
+    if (DTB_FENCE == 1) __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
-      __threadfence();
-      st_release(flags + blockIdx.x, epoch);
+      if (DTB_FENCE == 9) *(volatile int*)(flags + blockIdx.x) = epoch;
+      else st_release(flags + blockIdx.x, epoch);
     }
     DTB_MARK(t_pub)
     // 2. wait for the (up to 8) neighbours of this epoch
@@ -290,7 +412,16 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     __syncthreads();
     DTB_MARK(t_wait)
     // 3. refresh the halo ring (load region minus owned, domain ghost excluded)
-    g2s<T, K>(tile, xb, pitch, gx0, gy0, ring);
+    if (DTB_RING) {
+      refresh_ring<T, K>(tile, xb, pitch, gx0, gy0, ry0, oy0, oy1, ry1, rx0, ox0, ox1, rx1);
+    } else {
+      RectList<4> ring;
+      ring.set(0, ry0, oy0, rx0, rx1);
+      ring.set(1, oy1, ry1, rx0, rx1);
+      ring.set(2, oy0, oy1, rx0, ox0);
+      ring.set(3, oy0, oy1, ox1, rx1);
+      g2s<T, K>(tile, xb, pitch, gx0, gy0, ring);
+    }
     __syncthreads();
     DTB_MARK(t_ref)
   }

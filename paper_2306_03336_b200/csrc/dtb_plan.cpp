@@ -8,7 +8,7 @@
 
 namespace dtb {
 
-bool make_split(int N, int n, int h, int align, int maxL, int min_owned, Split& s) {
+bool make_split(int N, int n, int h, int align, int maxL, int min_owned, Split& s, int off) {
   s = Split();
   if (n < 1 || N < 1) return false;
   s.n = n;
@@ -37,7 +37,8 @@ bool make_split(int N, int n, int h, int align, int maxL, int min_owned, Split& 
   }
   for (int i = 0; i < n; ++i) {
     int L = s.l1[i] - s.l0[i];
-    int ext = (align - L % align) % align;
+    int ext = ((off - L) % align + align) % align;
+    if (ext && L + ext > maxL) ext = 0;  // keep within capacity (y: best effort)
     if (ext) {
       // grow the halo into a neighbour (never beyond that neighbour's owned cells)
       int rlim = (i + 1 < n) ? s.o1[i + 1] : N + 1;
@@ -48,7 +49,7 @@ bool make_split(int N, int n, int h, int align, int maxL, int min_owned, Split& 
       take = std::max(0, std::min(ext, s.l0[i] - llim));
       s.l0[i] -= take;
       ext -= take;
-      if (ext) s.dyn = true;
+      if (ext && off == 0) s.dyn = true;
     }
     s.max_load = std::max(s.max_load, s.l1[i] - s.l0[i]);
   }
@@ -138,7 +139,8 @@ bool plan_resident(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInf
         const int nty_max = (int)std::min<int64_t>(dev.sms / ntx, ny);
         for (int nty = nty_max; nty >= std::max(1, nty_max - 2); --nty) {
           Split sy;
-          if (!make_split((int)ny, nty, h, 1, maxRows, nty > 1 ? h : 1, sy)) continue;
+          // (L - 2) a multiple of 4 rows per band: the static sweep fast path
+          if (!make_split((int)ny, nty, h, 4 * W, maxRows, nty > 1 ? h : 1, sy, 2)) continue;
           // cost per epoch of hh steps: slowest CTA + exchange
           double cyc = tile_cycles(elem, K, W, sy.max_load, hh);
           if (steps > hh) {
@@ -194,7 +196,7 @@ bool plan_streaming(int64_t nx, int64_t ny, int elem, int64_t steps, const DevIn
           int nty = (int)std::max<int64_t>(1, (ny + 2 + maxRows - 1) / maxRows);
           Split sy;
           for (; nty <= ny; ++nty)
-            if (make_split((int)ny, nty, h, 1, maxRows, 1, sy)) break;
+            if (make_split((int)ny, nty, h, 4 * W, maxRows, 1, sy, 2)) break;
           if (nty > ny) continue;
           const int64_t ntiles = (int64_t)ntx * nty;
           const int64_t slots = (int64_t)dev.sms * occ;

@@ -60,7 +60,10 @@ struct Plan {
 // lane alignment `align` (load extents made multiples of it by growing the
 // halo into the neighbour, never past the ghost ring). Returns false if some
 // load extent exceeds maxL or a tile owns fewer than min_owned cells.
-bool make_split(int N, int n, int h, int align, int maxL, int min_owned, Split& s);
+// `align`/`off`: load extents are grown (when the neighbour has the cells)
+// to L = off (mod align); a miss is allowed in y (off != 0), flagged dyn in x.
+bool make_split(int N, int n, int h, int align, int maxL, int min_owned, Split& s,
+                int off = 0);
 
 // Choose the execution plan. force: 0 auto, 1 streaming, 2 naive.
 // depth > 0 pins the halo depth.
