@@ -168,6 +168,41 @@ __device__ __forceinline__ float lds_elem(uint32_t a, float) {
   return v;
 }
 
+// Whole-rectangle tile copies, one warp per row (coalesced along x, no
+// index division): tile rows [r0, r1) x cols [c0, c1) <-> global padded
+// (gy0 + r, gx0 + c). Loads are cp.async (the caller waits + syncs).
+template <typename T, int K>
+__device__ __forceinline__ void g2s_rows(T* tile, const T* __restrict__ g, int64_t pitch, int gx0,
+                                         int gy0, int r0, int r1, int c0, int c1) {
+  typedef Tile<T, K> L;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int r = r0 + warp; r < r1; r += nw) {
+    const T* src = g + (int64_t)(gy0 + r) * pitch + gx0;
+    const uint32_t srow = sbase + (uint32_t)(r * L::ROW * (int)sizeof(T));
+#pragma unroll 4
+    for (int c = c0 + lane; c < c1; c += 32)
+      cp_async(srow + (uint32_t)((L::swz(c / L::EPC) * L::EPC + c % L::EPC) * (int)sizeof(T)),
+               src + c);
+  }
+}
+
+template <typename T, int K>
+__device__ __forceinline__ void s2g_rows(const T* tile, T* __restrict__ g, int64_t pitch, int gx0,
+                                         int gy0, int r0, int r1, int c0, int c1) {
+  typedef Tile<T, K> L;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int r = r0 + warp; r < r1; r += nw) {
+    T* dst = g + (int64_t)(gy0 + r) * pitch + gx0;
+    const uint32_t srow = sbase + (uint32_t)(r * L::ROW * (int)sizeof(T));
+#pragma unroll 4
+    for (int c = c0 + lane; c < c1; c += 32)
+      dst[c] = lds_elem(srow + (uint32_t)((L::swz(c / L::EPC) * L::EPC + c % L::EPC) *
+                                          (int)sizeof(T)), T());
+  }
+}
+
 // Resident publish of the owned band: rows [oy0, t1) and [b0, oy1) in full
 // (one warp per row, coalesced), and the side columns [ox0, c1), [c2, ox1) of
 // the rows in between (one thread per row).
@@ -261,22 +296,16 @@ stream_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int
     const int4 cx = geo.col[tx], cy = geo.row[ty];
     const int Lw = cx.w - cx.z, Lh = cy.w - cy.z;
     // load region in padded coordinates = interior + 1
-    {
-      RectList<1> rl;
-      rl.set(0, 0, Lh, 0, Lw);
-      g2s<T, K>(tile, src, pitch, cx.z + 1, cy.z + 1, rl);
-    }
+    g2s_rows<T, K>(tile, src, pitch, cx.z + 1, cy.z + 1, 0, Lh, 0, Lw);
+    cp_async_wait_all();
     __syncthreads();
     advance<T, K, DYN>(tile, Lw, Lh, steps, wt, poison != 0, cx.z > -1, cx.w < nx + 1,
                        cy.z > -1, cy.w < ny + 1);
     // owned cells, plus the ghost ring where the tile touches the domain edge
     const int sx0 = cx.x - (cx.x == 0), sx1 = cx.y + (cx.y == nx);
     const int sy0 = cy.x - (cy.x == 0), sy1 = cy.y + (cy.y == ny);
-    {
-      RectList<1> rl;
-      rl.set(0, sy0 - cy.z, sy1 - cy.z, sx0 - cx.z, sx1 - cx.z);
-      s2g<T, K>(tile, dst, pitch, cx.z + 1, cy.z + 1, rl);
-    }
+    s2g_rows<T, K>(tile, dst, pitch, cx.z + 1, cy.z + 1, sy0 - cy.z, sy1 - cy.z, sx0 - cx.z,
+                   sx1 - cx.z);
     __syncthreads();
   }
 }
@@ -312,11 +341,8 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
   const int gx0 = cx.z + 1, gy0 = cy.z + 1;  // padded coords of tile (0,0)
   const bool hl = cx.z > -1, hr = cx.w < nx + 1, ht = cy.z > -1, hb = cy.w < ny + 1;
 
-  {
-    RectList<1> rl;
-    rl.set(0, 0, Lh, 0, Lw);
-    g2s<T, K>(tile, in, pitch, gx0, gy0, rl);
-  }
+  g2s_rows<T, K>(tile, in, pitch, gx0, gy0, 0, Lh, 0, Lw);
+  cp_async_wait_all();
   __syncthreads();
 
   // how deep each neighbour's load region reaches into my owned cells
@@ -430,11 +456,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     unsigned long long* tr = trace + 5 * blockIdx.x;
     tr[0] = t_comp; tr[1] = t_pub; tr[2] = t_wait; tr[3] = t_ref; tr[4] = epoch;
   }
-  {
-    RectList<1> rl;
-    rl.set(0, oy0 - !ht, oy1 + !hb, ox0 - !hl, ox1 + !hr);
-    s2g<T, K>(tile, out, pitch, gx0, gy0, rl);
-  }
+  s2g_rows<T, K>(tile, out, pitch, gx0, gy0, oy0 - !ht, oy1 + !hb, ox0 - !hl, ox1 + !hr);
 }
 
 // ---------------------------------------------------------------------------

@@ -92,25 +92,49 @@ double lanes_per_clk(int elem) { return elem == 8 ? 64.0 : 128.0; }
 // clock), so the non-FP instructions per row cost throughput there.
 double fp_efficiency(int elem) { return elem == 8 ? 0.92 : 0.80; }
 
-// SM cycles for one CTA to advance a (Lw x Lh) tile by `steps` steps.
+// Band heights exactly as the kernel splits them (dtb_core.cuh band_rows4 /
+// band_rows): two-step sweeps use whole 4-row quads per band (static fast
+// path), the last band takes the remainder (general path).
+static void band_heights(int rows, int nb, bool quads, std::vector<int>& hts) {
+  hts.assign(nb, 0);
+  const int q = rows / 4;
+  if (!quads || q < nb) {
+    for (int b = 0; b < nb; ++b) hts[b] = rows / nb + (b < rows % nb ? 1 : 0);
+    return;
+  }
+  for (int b = 0; b < nb; ++b) hts[b] = 4 * (q / nb + (b < q % nb ? 1 : 0));
+  hts[nb - 1] += rows - 4 * q;
+}
+
+// SM cycles for one CTA to advance a (Lw x Lh) tile by `steps` steps. Warp w
+// runs on sub-partition w % 4; a sweep lasts as long as the busiest
+// sub-partition's FP work (16 FP64 / 32 FP32 lanes per SMSP per clock).
 double tile_cycles(int elem, int K, int warps, int Lh, int steps) {
   const int rows = Lh - 2;
   if (rows <= 0 || steps <= 0) return 0;
-  const double row_cost = 32.0 * K * 9.0 / (lanes_per_clk(elem) * fp_efficiency(elem));
+  const double lane_rate = lanes_per_clk(elem) / 4.0 * fp_efficiency(elem);
+  const double row_cost = 32.0 * K * 9.0 / lane_rate;  // one warp-row on one SMSP
   double cyc = 0;
   int s = steps;
+  std::vector<int> hts;
   if (s >= 2 && rows >= 2) {
     const int nb = std::max(1, std::min(warps, rows / 2));
-    const int hb = (rows + nb - 1) / nb;
-    // each band: hb level-1 rows + 2 redundant seam rows + hb level-2 rows
-    const double sweep = nb * (2.0 * hb + 2.0) * row_cost + 400.0;  // + 2 barriers, fill
+    band_heights(rows, nb, true, hts);
+    double smsp[4] = {0, 0, 0, 0};
+    for (int b = 0; b < nb; ++b) {
+      const bool fast = hts[b] % 4 == 0 && hts[b] >= 4;
+      smsp[b % 4] += (2.0 * hts[b] + 2.0) * row_cost * (fast ? 1.0 : 1.25);
+    }
+    const double sweep = *std::max_element(smsp, smsp + 4) + 400.0;  // + barriers, fill
     cyc += (s / 2) * sweep;
     s %= 2;
   }
   if (s) {
     const int nb = std::max(1, std::min(warps, rows));
-    const int hb = (rows + nb - 1) / nb;
-    cyc += s * (nb * (double)hb * row_cost + 300.0);
+    band_heights(rows, nb, false, hts);
+    double smsp[4] = {0, 0, 0, 0};
+    for (int b = 0; b < nb; ++b) smsp[b % 4] += hts[b] * row_cost * 1.25;
+    cyc += s * (*std::max_element(smsp, smsp + 4) + 300.0);
   }
   return cyc;
 }
@@ -192,12 +216,13 @@ bool plan_streaming(int64_t nx, int64_t ny, int elem, int64_t steps, const DevIn
         for (int ntx = ntx_min; ntx <= ntx_min + 3 && ntx <= nx; ++ntx) {
           Split sx;
           if (!make_split((int)nx, ntx, h, K, Lw_max, 1, sx)) continue;
-          // tallest tiles that fit
-          int nty = (int)std::max<int64_t>(1, (ny + 2 + maxRows - 1) / maxRows);
+          // tallest tiles that fit, and a few shorter ones (band balance)
+          const int per_y = std::max(1, maxRows - 2 * h);
+          int nty0 = (int)std::max<int64_t>(
+              1, std::max<int64_t>((ny + 2 + maxRows - 1) / maxRows, (ny + per_y - 1) / per_y - 1));
+          for (int nty = nty0; nty <= std::min<int64_t>(ny, nty0 + 8); ++nty) {
           Split sy;
-          for (; nty <= ny; ++nty)
-            if (make_split((int)ny, nty, h, 4 * W, maxRows, 1, sy, 2)) break;
-          if (nty > ny) continue;
+          if (!make_split((int)ny, nty, h, 4 * W, maxRows, 1, sy, 2)) continue;
           const int64_t ntiles = (int64_t)ntx * nty;
           const int64_t slots = (int64_t)dev.sms * occ;
           const double waves = std::ceil((double)ntiles / slots);
@@ -225,6 +250,7 @@ bool plan_streaming(int64_t nx, int64_t ny, int elem, int64_t steps, const DevIn
             best.smem_bytes = (int64_t)sy.max_load * row_bytes;
             best.cycles_per_step = per_step;
             best.cells_per_clk = cpc;
+          }
           }
         }
       }
