@@ -115,8 +115,9 @@ int dtb_plan(int64_t nx, int64_t ny, int32_t elem_bytes, int64_t total_steps,
 
 /* Phase counters of the most recent DTB_FLAG_TRACE resident solve on this
  * thread: for each CTA, SM clock cycles spent in {compute, publish, wait,
- * refresh} plus the epoch count (5 values per CTA). Copies up to n values
- * into out and returns the number of CTAs (0 if no trace). */
+ * refresh}, the epoch count, and the publish split {stores, barrier} (8 values
+ * per CTA, the last unused). Copies up to n values into out and returns the
+ * number of CTAs (0 if no trace). */
 int64_t dtb_last_trace(int64_t* out, int64_t n);
 
 /* Kernel launches issued by the most recent solve on this thread. */

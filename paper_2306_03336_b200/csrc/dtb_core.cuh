@@ -47,7 +47,8 @@
                         // inside the last sweep, 2 each warp right after its own last sweep
 #endif
 #ifndef DTB_RING
-#define DTB_RING 1      // resident: specialised cp.async halo refresh
+#define DTB_RING 2      // resident halo refresh: 0 generic, 1 ring copy after one wait,
+                        // 2 warp per direction: poll that neighbour, then copy its region
 #endif
 
 namespace dtb {

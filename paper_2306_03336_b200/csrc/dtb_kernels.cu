@@ -203,6 +203,66 @@ __device__ __forceinline__ void s2g_rows(const T* tile, T* __restrict__ g, int64
   }
 }
 
+// Halo refresh, warp-specialised by direction: region k (N, S, W, E, NW, NE,
+// SW, SE) of the ring is owned by one neighbour; warp k polls that
+// neighbour's epoch flag and streams the region in with cp.async as soon as
+// it is published, so the eight waits and loads overlap.
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename T, int K>
+__device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restrict__ g,
+                                                     int64_t pitch, int gx0, int gy0,
+                                                     const int* flags, int epoch, int ntx, int nty,
+                                                     int tx, int ty, int ry0, int oy0, int oy1,
+                                                     int ry1, int rx0, int ox0, int ox1, int rx1) {
+  typedef Tile<T, K> L;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int k = warp; k < 8; k += nw) {
+    int dx, dy, r0, r1, c0, c1;
+    switch (k) {
+      case 0: dx = 0; dy = -1; r0 = ry0; r1 = oy0; c0 = ox0; c1 = ox1; break;
+      case 1: dx = 0; dy = 1; r0 = oy1; r1 = ry1; c0 = ox0; c1 = ox1; break;
+      case 2: dx = -1; dy = 0; r0 = oy0; r1 = oy1; c0 = rx0; c1 = ox0; break;
+      case 3: dx = 1; dy = 0; r0 = oy0; r1 = oy1; c0 = ox1; c1 = rx1; break;
+      case 4: dx = -1; dy = -1; r0 = ry0; r1 = oy0; c0 = rx0; c1 = ox0; break;
+      case 5: dx = 1; dy = -1; r0 = ry0; r1 = oy0; c0 = ox1; c1 = rx1; break;
+      case 6: dx = -1; dy = 1; r0 = oy1; r1 = ry1; c0 = rx0; c1 = ox0; break;
+      default: dx = 1; dy = 1; r0 = oy1; r1 = ry1; c0 = ox1; c1 = rx1; break;
+    }
+    const int nxt = tx + dx, nyt = ty + dy;
+    if (r1 <= r0 || c1 <= c0 || nxt < 0 || nxt >= ntx || nyt < 0 || nyt >= nty) continue;
+    if (lane == 0) {
+      const int* f = flags + nyt * ntx + nxt;
+      while (ld_acquire_gpu(f) < epoch) __nanosleep(32);
+    }
+    __syncwarp();
+    if (c1 - c0 >= 16) {  // wide region: lanes across columns
+      for (int r = r0; r < r1; ++r) {
+        const T* src = g + (int64_t)(gy0 + r) * pitch + gx0;
+        const uint32_t srow = sbase + (uint32_t)(r * L::ROW * (int)sizeof(T));
+        for (int c = c0 + lane; c < c1; c += 32)
+          cp_async(srow + (uint32_t)((L::swz(c / L::EPC) * L::EPC + c % L::EPC) * (int)sizeof(T)),
+                   src + c);
+      }
+    } else {  // narrow region: flattened, column-fastest (few sectors per warp load)
+      const int w = c1 - c0, n = (r1 - r0) * w;
+      const uint32_t m = (65535u + w) / w;
+      for (int i = lane; i < n; i += 32) {
+        const uint32_t q = ((uint32_t)i * m) >> 16;
+        const int r = r0 + (int)q, c = c0 + i - (int)q * w;
+        cp_async(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)),
+                 g + (int64_t)(gy0 + r) * pitch + gx0 + c);
+      }
+    }
+  }
+  cp_async_wait_all();
+}
+
 // Resident publish of the owned band: rows [oy0, t1) and [b0, oy1) in full
 // (one warp per row, coalesced), and the side columns [ox0, c1), [c2, ox1) of
 // the rows in between (one thread per row).
@@ -221,12 +281,23 @@ __device__ __forceinline__ void publish_band(const T* tile, T* __restrict__ g, i
     for (int c = ox0 + lane; c < ox1; c += 32)
       dst[c] = lds_elem(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)), T());
   }
-  for (int r = t1 + threadIdx.x; r < b0; r += blockDim.x) {
-    T* dst = g + (int64_t)(gy0 + r) * pitch + gx0;
-    for (int c = ox0; c < c1; ++c)
-      dst[c] = lds_elem(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)), T());
-    for (int c = c2; c < ox1; ++c)
-      dst[c] = lds_elem(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)), T());
+  // side columns, flattened column-fastest so a warp's stores hit few sectors
+  const int wl = c1 - ox0, wr = ox1 - c2, nr = b0 - t1;
+  const int nl = wl > 0 ? nr * wl : 0, ntot = nl + (wr > 0 ? nr * wr : 0);
+  const uint32_t ml = wl > 0 ? (65535u + wl) / wl : 0, mr = wr > 0 ? (65535u + wr) / wr : 0;
+  for (int i = threadIdx.x; i < ntot; i += blockDim.x) {
+    int r, c;
+    if (i < nl) {
+      const uint32_t q = ((uint32_t)i * ml) >> 16;
+      r = t1 + (int)q;
+      c = ox0 + i - (int)q * wl;
+    } else {
+      const uint32_t j = (uint32_t)(i - nl), q = (j * mr) >> 16;
+      r = t1 + (int)q;
+      c = c2 + (int)j - (int)q * wr;
+    }
+    g[(int64_t)(gy0 + r) * pitch + gx0 + c] =
+        lds_elem(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)), T());
   }
 }
 
@@ -357,7 +428,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
 
   int64_t done = 0;
   int epoch = 0;
-  unsigned long long t_comp = 0, t_pub = 0, t_wait = 0, t_ref = 0, tc = 0;
+  unsigned long long t_comp = 0, t_pub = 0, t_wait = 0, t_ref = 0, t_pst = 0, t_pbar = 0, tc = 0;
   const bool tracing = trace != nullptr && threadIdx.x == 0;
   if (tracing) tc = clock64();
 #define DTB_MARK(acc)                                  \
@@ -419,13 +490,23 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
 #define DTB_FENCE 0  // 0: thread 0 st.release after the barrier; 1: every thread fences first;
                      // 9: no fence (timing experiments only - unsynchronised)
 #endif
+    DTB_MARK(t_pst)
     if (DTB_FENCE == 1) __threadfence();
     __syncthreads();
+    DTB_MARK(t_pbar)
     if (threadIdx.x == 0) {
       if (DTB_FENCE == 9) *(volatile int*)(flags + blockIdx.x) = epoch;
       else st_release(flags + blockIdx.x, epoch);
     }
     DTB_MARK(t_pub)
+    if (DTB_RING == 2) {
+      // 2+3. per-direction: warp k waits for the neighbour owning halo region k
+      // and immediately streams that region in (overlaps the 8 waits and loads)
+      DTB_MARK(t_wait)
+      refresh_by_direction<T, K>(tile, xb, pitch, gx0, gy0, flags, epoch, geo.ntx, geo.nty, tx,
+                                 ty, ry0, oy0, oy1, ry1, rx0, ox0, ox1, rx1);
+      __syncthreads();
+    } else {
     // 2. wait for the (up to 8) neighbours of this epoch
     if (threadIdx.x < 9 && threadIdx.x != 4) {
       const int dx = (int)threadIdx.x % 3 - 1, dy = (int)threadIdx.x / 3 - 1;
@@ -449,12 +530,14 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
       g2s<T, K>(tile, xb, pitch, gx0, gy0, ring);
     }
     __syncthreads();
+    }
     DTB_MARK(t_ref)
   }
 #undef DTB_MARK
   if (tracing) {
-    unsigned long long* tr = trace + 5 * blockIdx.x;
+    unsigned long long* tr = trace + 8 * blockIdx.x;
     tr[0] = t_comp; tr[1] = t_pub; tr[2] = t_wait; tr[3] = t_ref; tr[4] = epoch;
+    tr[5] = t_pst; tr[6] = t_pbar;
   }
   s2g_rows<T, K>(tile, out, pitch, gx0, gy0, oy0 - !ht, oy1 + !hb, ox0 - !hl, ox1 + !hr);
 }
@@ -614,7 +697,7 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
                   p.ctas, per_sm * sms);
     void* scratch = nullptr;
     const size_t flag_bytes = 256 + (size_t)p.ctas * sizeof(int);
-    const size_t trace_bytes = (size_t)p.ctas * 5 * sizeof(unsigned long long);
+    const size_t trace_bytes = (size_t)p.ctas * 8 * sizeof(unsigned long long);
     {
       std::lock_guard<std::mutex> lk(g_mu);
       int rc = arena_get(g_scratch[device & 15], 2 * grid_bytes + flag_bytes + trace_bytes + 256,
@@ -641,7 +724,7 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
     if (tracing) {
-      std::vector<unsigned long long> h_tr((size_t)p.ctas * 5);
+      std::vector<unsigned long long> h_tr((size_t)p.ctas * 8);
       CUDA_TRY(cudaMemcpyAsync(h_tr.data(), trace, trace_bytes, cudaMemcpyDeviceToHost, st));
       CUDA_TRY(cudaStreamSynchronize(st));
       g_trace.assign(h_tr.begin(), h_tr.end());
@@ -691,8 +774,14 @@ int dispatch(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_
     return dispatch_dyn<T, KK, WW>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st);
   if constexpr (sizeof(T) == 8) {
     DTB_SHAPE(4, 8)
+#ifdef DTB_WIDE
+    DTB_SHAPE(8, 8)
+#endif
   } else {
     DTB_SHAPE(8, 8)
+#ifdef DTB_WIDE
+    DTB_SHAPE(16, 8)
+#endif
   }
 #undef DTB_SHAPE
   return fail(DTB_EINFEASIBLE, "no kernel instance for elem %d K %d warps %d", (int)sizeof(T),
@@ -949,7 +1038,7 @@ int64_t dtb_last_launch_count(void) { return g_launches; }
 int64_t dtb_last_trace(int64_t* out, int64_t n) {
   const int64_t m = std::min<int64_t>(n, (int64_t)g_trace.size());
   for (int64_t i = 0; i < m && out; ++i) out[i] = g_trace[(size_t)i];
-  return (int64_t)g_trace.size() / 5;
+  return (int64_t)g_trace.size() / 8;
 }
 
 int dtb_device_info(int32_t* sms, int64_t* smem_optin_per_block, int64_t* l2_bytes,

@@ -39,13 +39,14 @@ if __name__ == "__main__":
             j2d5pt_device(a, b, nx, ny, StencilWeights.diffusive(0.2), steps,
                           flags=flags | _native.FLAG_TRACE, depth=depth)
             torch.cuda.synchronize()
-            buf = (ctypes.c_int64 * (5 * 200))()
-            n = _native.lib().dtb_last_trace(buf, 5 * 200)
-            v = [list(buf[5 * i:5 * i + 5]) for i in range(n)]
-            tot = [sum(x[k] for x in v) / n for k in range(5)]
+            buf = (ctypes.c_int64 * (8 * 200))()
+            n = _native.lib().dtb_last_trace(buf, 8 * 200)
+            v = [list(buf[8 * i:8 * i + 8]) for i in range(n)]
+            tot = [sum(x[k] for x in v) / n for k in range(8)]
             cyc = sum(tot[:4])
             extra = {"trace_frac": {k: round(tot[i] / cyc, 3) for i, k in
                                     enumerate(["compute", "publish", "wait", "refresh"])},
+                     "publish_split": {"stores": round(tot[5] / cyc, 3), "barrier": round(tot[6] / cyc, 3)},
                      "cycles_per_epoch": round(cyc / max(tot[4], 1)),
                      "compute_cycles_per_step_max": round(max(x[0] for x in v) / steps),
                      "compute_cycles_per_step_min": round(min(x[0] for x in v) / steps)}
