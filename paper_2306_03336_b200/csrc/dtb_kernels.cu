@@ -168,22 +168,39 @@ __device__ __forceinline__ float lds_elem(uint32_t a, float) {
   return v;
 }
 
-// Whole-rectangle tile copies, one warp per row (coalesced along x, no
-// index division): tile rows [r0, r1) x cols [c0, c1) <-> global padded
-// (gy0 + r, gx0 + c). Loads are cp.async (the caller waits + syncs).
+// Whole-rectangle tile copies, one warp per row, one 16-byte smem chunk per
+// lane-iteration (the swizzled chunk address is computed once per chunk):
+// tile rows [r0, r1) x cols [c0, c1) <-> global padded (gy0 + r, gx0 + c).
+// When the global side is 16-byte aligned chunk-for-chunk (gx0 and pitch
+// multiples of the chunk), whole chunks move as one 16-byte cp.async / STG;
+// otherwise element by element. Loads are cp.async (caller waits + syncs).
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+
 template <typename T, int K>
 __device__ __forceinline__ void g2s_rows(T* tile, const T* __restrict__ g, int64_t pitch, int gx0,
                                          int gy0, int r0, int r1, int c0, int c1) {
   typedef Tile<T, K> L;
+  constexpr int E = L::EPC;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const bool vec = ((gx0 % E) == 0) && ((pitch % E) == 0);
+  const int q0 = c0 / E, q1 = (c1 + E - 1) / E;
   for (int r = r0 + warp; r < r1; r += nw) {
     const T* src = g + (int64_t)(gy0 + r) * pitch + gx0;
     const uint32_t srow = sbase + (uint32_t)(r * L::ROW * (int)sizeof(T));
-#pragma unroll 4
-    for (int c = c0 + lane; c < c1; c += 32)
-      cp_async(srow + (uint32_t)((L::swz(c / L::EPC) * L::EPC + c % L::EPC) * (int)sizeof(T)),
-               src + c);
+    for (int q = q0 + lane; q < q1; q += 32) {
+      const uint32_t sa = srow + (uint32_t)(L::swz(q) * 16);
+      const int cb = q * E;
+      if (vec && cb >= c0 && cb + E <= c1) {
+        cp_async16(sa, src + cb);
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          if (cb + e >= c0 && cb + e < c1) cp_async(sa + (uint32_t)(e * sizeof(T)), src + cb + e);
+      }
+    }
   }
 }
 
@@ -191,15 +208,26 @@ template <typename T, int K>
 __device__ __forceinline__ void s2g_rows(const T* tile, T* __restrict__ g, int64_t pitch, int gx0,
                                          int gy0, int r0, int r1, int c0, int c1) {
   typedef Tile<T, K> L;
-  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
+  typedef typename Arith<T>::vec_t V;
+  constexpr int E = L::EPC;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const bool vec = ((gx0 % E) == 0) && ((pitch % E) == 0);
+  const int q0 = c0 / E, q1 = (c1 + E - 1) / E;
   for (int r = r0 + warp; r < r1; r += nw) {
     T* dst = g + (int64_t)(gy0 + r) * pitch + gx0;
-    const uint32_t srow = sbase + (uint32_t)(r * L::ROW * (int)sizeof(T));
-#pragma unroll 4
-    for (int c = c0 + lane; c < c1; c += 32)
-      dst[c] = lds_elem(srow + (uint32_t)((L::swz(c / L::EPC) * L::EPC + c % L::EPC) *
-                                          (int)sizeof(T)), T());
+    const T* srow = tile + r * L::ROW;
+    for (int q = q0 + lane; q < q1; q += 32) {
+      const V x = *reinterpret_cast<const V*>(srow + L::swz(q) * E);
+      const T* px = reinterpret_cast<const T*>(&x);
+      const int cb = q * E;
+      if (vec && cb >= c0 && cb + E <= c1) {
+        *reinterpret_cast<V*>(dst + cb) = x;
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          if (cb + e >= c0 && cb + e < c1) dst[cb + e] = px[e];
+      }
+    }
   }
 }
 
@@ -355,21 +383,44 @@ __device__ void advance(T* tile, int Lw, int Lh, int steps, const Weights<T>& wt
 // ---------------------------------------------------------------------------
 // streaming: one pass of h fused steps over every tile
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// One HBM pass over every tile. nbuf == 2: the CTA's smem holds two tile
+// buffers; tile i+1 streams in (cp.async) while tile i is advanced and
+// stored, so HBM traffic overlaps the FP64/FP32 work. nbuf == 1: tall tiles,
+// load / compute / store in sequence.
 template <typename T, int K, int NW, bool DYN>
 __global__ void __launch_bounds__(NW * 32, 1)
 stream_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int nx, int ny,
-              Weights<T> wt, int steps, int poison, const __grid_constant__ Geometry geo) {
+              Weights<T> wt, int steps, int poison, int nbuf, int buf_elems,
+              const __grid_constant__ Geometry geo) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* tile = reinterpret_cast<T*>(smem_raw);
+  T* bufs[2] = {reinterpret_cast<T*>(smem_raw), reinterpret_cast<T*>(smem_raw) + buf_elems};
   const int ntiles = geo.ntx * geo.nty;
-  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  auto issue_load = [&](int t, T* tile) {
+    const int tx = t % geo.ntx, ty = t / geo.ntx;
+    const int4 cx = geo.col[tx], cy = geo.row[ty];
+    g2s_rows<T, K>(tile, src, pitch, cx.z + 1, cy.z + 1, 0, cy.w - cy.z, 0, cx.w - cx.z);
+  };
+  int i = 0;
+  if (nbuf == 2 && (int)blockIdx.x < ntiles) issue_load(blockIdx.x, bufs[0]);
+  cp_async_commit();
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+    T* tile = bufs[nbuf == 2 ? (i & 1) : 0];
+    if (nbuf == 2) {
+      const int tn = t + gridDim.x;
+      if (tn < ntiles) issue_load(tn, bufs[(i + 1) & 1]);  // prefetch the next tile
+      cp_async_commit();
+      cp_async_wait_1();  // this tile's copies have landed
+    } else {
+      issue_load(t, tile);
+      cp_async_wait_all();
+    }
+    __syncthreads();
     const int tx = t % geo.ntx, ty = t / geo.ntx;
     const int4 cx = geo.col[tx], cy = geo.row[ty];
     const int Lw = cx.w - cx.z, Lh = cy.w - cy.z;
-    // load region in padded coordinates = interior + 1
-    g2s_rows<T, K>(tile, src, pitch, cx.z + 1, cy.z + 1, 0, Lh, 0, Lw);
-    cp_async_wait_all();
-    __syncthreads();
     advance<T, K, DYN>(tile, Lw, Lh, steps, wt, poison != 0, cx.z > -1, cx.w < nx + 1,
                        cy.z > -1, cy.w < ny + 1);
     // owned cells, plus the ghost ring where the tile touches the domain edge
@@ -377,8 +428,9 @@ stream_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int
     const int sy0 = cy.x - (cy.x == 0), sy1 = cy.y + (cy.y == ny);
     s2g_rows<T, K>(tile, dst, pitch, cx.z + 1, cy.z + 1, sy0 - cy.z, sy1 - cy.z, sx0 - cx.z,
                    sx1 - cx.z);
-    __syncthreads();
+    __syncthreads();  // every read of this buffer is done before it is refilled
   }
+  cp_async_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -733,7 +785,8 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
   }
   // streaming passes, ping-ponging dst between out and a scratch grid
   auto kern = stream_kernel<T, K, NW, DYN>;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem * p.ctas_per_sm));
   const int64_t passes = (steps + p.h - 1) / p.h;
   T* tmp = nullptr;
   if (passes > 1) {
@@ -745,10 +798,13 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
   }
   const T* src = d_in;
   int64_t done = 0;
+  const int nbuf = p.ctas_per_sm;  // the planner's occupancy 2 == double-buffered CTA
+  const int buf_elems = (int)(p.smem_bytes / (int64_t)sizeof(T));
   for (int64_t i = 0; i < passes; ++i) {
     const int s = (int)std::min<int64_t>(p.h, steps - done);
     T* dst = ((passes - 1 - i) % 2 == 0) ? d_out : tmp;
-    kern<<<p.ctas, threads, smem, st>>>(src, dst, pitch, nx, ny, wt, s, poison ? 1 : 0, geo);
+    kern<<<p.ctas, threads, (size_t)smem * nbuf, st>>>(src, dst, pitch, nx, ny, wt, s,
+                                                       poison ? 1 : 0, nbuf, buf_elems, geo);
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
     src = dst;

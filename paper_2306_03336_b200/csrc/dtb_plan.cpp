@@ -203,9 +203,9 @@ bool plan_streaming(int64_t nx, int64_t ny, int elem, int64_t steps, const DevIn
     const int K = sh.K, W = sh.warps;
     const int Lw_max = 32 * K;
     const int64_t row_bytes = (int64_t)Lw_max * elem;
-    for (int occ = 1; occ <= 2; ++occ) {
-      const int64_t smem_cta = std::min<int64_t>(dev.smem_optin, dev.smem_per_sm / occ - 1024);
-      const int maxRows = (int)((smem_cta - 1024) / row_bytes);
+    for (int occ = 1; occ <= 2; ++occ) {  // occ = tile buffers per CTA (2: double-buffered)
+      const int64_t smem_cta = (dev.smem_optin - 1024) / occ;
+      const int maxRows = (int)(smem_cta / row_bytes);
       if (maxRows < 8) continue;
       for (int h : depths_for(depth)) {
         const int hh = (int)std::min<int64_t>(h, std::max<int64_t>(steps, 1));
@@ -224,16 +224,16 @@ bool plan_streaming(int64_t nx, int64_t ny, int elem, int64_t steps, const DevIn
           Split sy;
           if (!make_split((int)ny, nty, h, 4 * W, maxRows, 1, sy, 2)) continue;
           const int64_t ntiles = (int64_t)ntx * nty;
-          const int64_t slots = (int64_t)dev.sms * occ;
+          const int64_t slots = dev.sms;  // one CTA per SM
           const double waves = std::ceil((double)ntiles / slots);
           const double tc = tile_cycles(elem, K, W, sy.max_load, hh);
           const double load_b = (double)sx.max_load * sy.max_load * elem;
           const double store_b = (double)(sx.max_load - 2 * h) * (sy.max_load - 2 * h) * elem;
-          // per-CTA memory time at its share of HBM bandwidth
+          // per-tile memory time at this SM's share of HBM bandwidth
           const double mem_cta = (load_b + store_b) / (kHbmBytesPerClk / slots);
-          // a wave = occ tiles per SM sharing its FP pipe; one CTA's load/store
-          // overlaps the other CTAs' compute when occ >= 2
-          const double pass = waves * std::max(occ * tc, mem_cta + tc) + 6000.0;
+          // double-buffered: the next tile's load overlaps this tile's compute
+          const double per_tile = occ == 2 ? std::max(tc, mem_cta) + 500.0 : tc + mem_cta;
+          const double pass = waves * per_tile + mem_cta + 6000.0;
           const double per_step = pass / hh;
           const double cpc = (double)nx * ny / per_step;
           if (!found || cpc > best.cells_per_clk) {
@@ -246,7 +246,7 @@ bool plan_streaming(int64_t nx, int64_t ny, int elem, int64_t steps, const DevIn
             best.sx = sx;
             best.sy = sy;
             best.ctas = (int)std::min<int64_t>(ntiles, slots);
-            best.ctas_per_sm = occ;
+            best.ctas_per_sm = occ;  // streaming: tile buffers per CTA
             best.smem_bytes = (int64_t)sy.max_load * row_bytes;
             best.cycles_per_step = per_step;
             best.cells_per_clk = cpc;
