@@ -35,6 +35,9 @@ WORKLOADS = {
     "c3a": (2700, 2700, 10000, "f32", "j2d5pt fp32 2700x2700, 10000 steps, smem-resident (BASELINE config 3)"),
     "c3b": (8192, 8192, 1000, "f32", "j2d5pt fp32 8192x8192, 1000 steps, streaming (BASELINE config 3)"),
     "c4": (16384, 16384, 1000, "f64", "j2d5pt fp64 16384x16384, 1000 steps, streaming (BASELINE config 4)"),
+    # C5 weak-scaling series: 32768 x (4096 * N) fp64 y-slabs, depth-16 halo exchange
+    "c5": (32768, 4096, 1000, "f64", "j2d5pt fp64 32768x(4096*N) y-slabs, 1000 steps, depth-16 "
+                                     "NVLink halo exchange (BASELINE config 5, weak scaling)"),
 }
 
 METRIC = "j2d5pt GCells/s (fp64/fp32) at 1/2/4/8 B200 vs roofline and CPU reference"
@@ -185,6 +188,94 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_slab(args, world, rank, local):
+    """C5: one y-slab per rank (SlabSolver), halo rows exchanged point-to-point
+    over NCCL every `depth` steps; weak scaling (4096 rows per GPU)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2306_03336_b200 import StencilWeights, j2d5pt_device, last_launch_count
+    from paper_2306_03336_b200.prng import fill_random_rows_device
+    from paper_2306_03336_b200.slab import SlabGeometry, SlabSolver
+    nx, rows_per_gpu, steps, dtype, desc = WORKLOADS["c5"]
+    if args.solve_steps:
+        steps = args.solve_steps
+    ny = rows_per_gpu * world
+    depth = 16
+    dev = torch.device("cuda", local)
+    geo = SlabGeometry(nx, ny, world, rank, depth)
+    pitch = (nx + 2 + 31) // 32 * 32
+    a = torch.empty((geo.local_ny + 2, pitch), dtype=torch.float64, device=dev)
+    b = torch.empty_like(a)
+    w = StencilWeights.diffusive(0.2)
+    launches = [0]
+
+    def local_solve(src, dst, lnx, lny, k):
+        j2d5pt_device(src, dst, lnx, lny, w, k)
+        launches[0] += last_launch_count()
+
+    solver = SlabSolver(geo, local_solve, dist if world > 1 else None)
+
+    def fresh():
+        fill_random_rows_device(a, nx, ny, 1, geo.global_row0)
+        solver.attach(a, b)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        fresh()
+        solver.run(steps)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    total_ms = 0.0
+    launches[0] = 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            fresh()
+            torch.cuda.synchronize()
+            barrier()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            solver.run(steps)
+            e.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            total_ms += s.elapsed_time(e)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    cells = nx * ny * steps  # whole job
+    value = cells * args.steps / (total_ms * 1e-3) / 1e9
+    if rank != 0:
+        return
+    peaks = measured_peaks()
+    per_gpu = value / world
+    rooflines = {
+        "fp_pipe": {"achieved": per_gpu * 9, "peak": peaks["fp64_gops"], "unit": "Gop/s",
+                    "ops_per_cell": 9},
+    }
+    rooflines["fp_pipe"]["frac"] = rooflines["fp_pipe"]["achieved"] / rooflines["fp_pipe"]["peak"]
+    halo_bytes = 2 * depth * (nx + 2) * 8 * (2 if world > 2 else 1)
+    line = {
+        "metric": METRIC, "value": value, "unit": "GCells/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+        "data": "synthetic (splitmix64 random_interior seed 1, each slab filled on its GPU)",
+        "config": {"workload": desc, "nx": nx, "ny": ny, "solve_steps": steps, "depth": depth,
+                   "parallelism": f"y-slab x{world}", "l2": "inputs (>= 1 GB) larger than L2"},
+        "roofline": dict(rooflines["fp_pipe"], bound="fp64_pipe", traffic=None),
+        "rooflines": rooflines,
+        "nvlink_halo_bytes_per_exchange_per_gpu": halo_bytes if world > 1 else 0,
+        "gpu_launches": launches[0],
+        "clocks": clk.summary(),
+        "e2e": None,
+        "cpu_baseline": cpu_reference_sample(nx, 256, dtype) if not args.no_cpu else None,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_b200(args):
     import numpy as np
     import torch
@@ -192,7 +283,9 @@ def run_b200(args):
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if world > 1 or args.workload == "c5":
+        return run_slab(args, world, rank, local)
     from paper_2306_03336_b200 import StencilWeights, j2d5pt_device, last_launch_count, plan_b200
     from paper_2306_03336_b200 import _native
     from paper_2306_03336_b200.prng import fill_random_device
@@ -324,6 +417,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--solve-steps", type=int, default=0,
+                    help="override the workload's Jacobi step count (quick runs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)  # the timing rules require >= 3 warm-up steps
     if args.impl == "reference":

@@ -134,6 +134,12 @@ int dtb_fill_random_f64(double* d_out, int64_t nx, int64_t ny, int64_t pitch,
 int dtb_fill_random_f32(float* d_out, int64_t nx, int64_t ny, int64_t pitch,
                         uint64_t seed, double ghost, void* stream);
 
+/* Rows [row0, row0 + nrows) of that padded grid only, written from d_out's
+ * first row (a multi-GPU slab fills its own rows without the full grid). */
+int dtb_fill_random_rows_f64(double* d_out, int64_t nx, int64_t ny, int64_t pitch,
+                             uint64_t seed, double ghost, int64_t row0, int64_t nrows,
+                             void* stream);
+
 /* Last error message on this thread ("" if none). */
 const char* dtb_last_error(void);
 

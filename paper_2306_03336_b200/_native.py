@@ -90,6 +90,8 @@ _SIGNATURES = {
                                     c_void_p]),
     "dtb_fill_random_f32": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_uint64, c_double,
                                     c_void_p]),
+    "dtb_fill_random_rows_f64": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_uint64, c_double,
+                                         c_int64, c_int64, c_void_p]),
     "dtb_last_error": (c_char_p, []),
 }
 

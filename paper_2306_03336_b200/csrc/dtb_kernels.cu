@@ -615,13 +615,14 @@ __global__ void naive_kernel(const T* __restrict__ a, T* __restrict__ b, int64_t
 // ---------------------------------------------------------------------------
 // splitmix64 fill (prng.py:45-67): interior (x, y) = value i = y*nx + x
 // ---------------------------------------------------------------------------
+// Rows [row0, row0 + nrows) of the padded global grid, written to out[0..].
 template <typename T>
 __global__ void fill_random_kernel(T* out, int64_t pitch, int nx, int ny, uint64_t seed,
-                                   double ghost) {
-  const int64_t total = (int64_t)(nx + 2) * (ny + 2);
+                                   double ghost, int64_t row0, int64_t nrows) {
+  const int64_t total = (int64_t)(nx + 2) * nrows;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
        k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t y = k / (nx + 2), x = k % (nx + 2);
+    const int64_t yl = k / (nx + 2), x = k % (nx + 2), y = row0 + yl;
     double v;
     if (x == 0 || y == 0 || x == nx + 1 || y == ny + 1) {
       v = ghost;
@@ -633,7 +634,7 @@ __global__ void fill_random_kernel(T* out, int64_t pitch, int nx, int ny, uint64
       z = z ^ (z >> 31);
       v = (double)(z >> 11) * (1.0 / 9007199254740992.0);
     }
-    out[y * pitch + x] = (T)v;
+    out[yl * pitch + x] = (T)v;
   }
 }
 
@@ -1119,7 +1120,7 @@ int dtb_fill_random_f64(double* d_out, int64_t nx, int64_t ny, int64_t pitch, ui
                         double ghost, void* stream) {
   g_err.clear();
   if (nx < 1 || ny < 1 || pitch < nx + 2) return fail(DTB_EINVAL, "bad fill dims");
-  fill_random_kernel<double><<<1184, 256, 0, (cudaStream_t)stream>>>(d_out, pitch, (int)nx, (int)ny, seed, ghost);
+  fill_random_kernel<double><<<1184, 256, 0, (cudaStream_t)stream>>>(d_out, pitch, (int)nx, (int)ny, seed, ghost, 0, ny + 2);
   CUDA_TRY(cudaGetLastError());
   return DTB_OK;
 }
@@ -1128,7 +1129,18 @@ int dtb_fill_random_f32(float* d_out, int64_t nx, int64_t ny, int64_t pitch, uin
                         double ghost, void* stream) {
   g_err.clear();
   if (nx < 1 || ny < 1 || pitch < nx + 2) return fail(DTB_EINVAL, "bad fill dims");
-  fill_random_kernel<float><<<1184, 256, 0, (cudaStream_t)stream>>>(d_out, pitch, (int)nx, (int)ny, seed, ghost);
+  fill_random_kernel<float><<<1184, 256, 0, (cudaStream_t)stream>>>(d_out, pitch, (int)nx, (int)ny, seed, ghost, 0, ny + 2);
+  CUDA_TRY(cudaGetLastError());
+  return DTB_OK;
+}
+
+int dtb_fill_random_rows_f64(double* d_out, int64_t nx, int64_t ny, int64_t pitch, uint64_t seed,
+                             double ghost, int64_t row0, int64_t nrows, void* stream) {
+  g_err.clear();
+  if (nx < 1 || ny < 1 || pitch < nx + 2 || row0 < 0 || nrows < 0 || row0 + nrows > ny + 2)
+    return fail(DTB_EINVAL, "bad fill rows");
+  fill_random_kernel<double><<<1184, 256, 0, (cudaStream_t)stream>>>(d_out, pitch, (int)nx, (int)ny,
+                                                                    seed, ghost, row0, nrows);
   CUDA_TRY(cudaGetLastError());
   return DTB_OK;
 }

@@ -48,3 +48,17 @@ def fill_random_device(buf, nx: int, ny: int, seed: int, ghost: float = 0.0, str
             ctypes.c_void_p(stream))
     if rc != 0:
         raise RuntimeError(_native.last_error())
+
+
+def fill_random_rows_device(buf, nx: int, ny: int, seed: int, row0: int, ghost: float = 0.0,
+                            stream=None):
+    """Rows [row0, row0 + buf.shape[0]) of the padded fp64 random grid into ``buf``."""
+    import torch
+    from . import _native
+    if stream is None:
+        stream = torch.cuda.current_stream(buf.device).cuda_stream
+    rc = _native.lib().dtb_fill_random_rows_f64(buf.data_ptr(), nx, ny, buf.stride(0),
+                                                 seed & (2 ** 64 - 1), float(ghost), row0,
+                                                 buf.shape[0], ctypes.c_void_p(stream))
+    if rc != 0:
+        raise RuntimeError(_native.last_error())
