@@ -241,6 +241,38 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   return v;
 }
 
+// Copy tile rect [r0, r1) x [c0, c1) from global by 16-byte smem chunks,
+// flattened over (row, chunk) across the 32 lanes of one warp. Whole chunks
+// use a 16-byte cp.async when the global side is aligned (vec).
+template <typename T, int K>
+__device__ __forceinline__ void warp_g2s_chunks(uint32_t sbase, const T* __restrict__ g,
+                                                int64_t pitch, int gx0, int gy0, int r0, int r1,
+                                                int c0, int c1, bool vec, int lane) {
+  typedef Tile<T, K> L;
+  constexpr int E = L::EPC;
+  const int q0 = c0 / E, nq = (c1 + E - 1) / E - q0, n = (r1 - r0) * nq;
+  if (n <= 0) return;
+  const uint64_t m = (0xFFFFFFFFull + (uint64_t)nq) / (uint64_t)nq;
+  for (int i = lane; i < n; i += 32) {
+    const uint32_t rr = (uint32_t)(((uint64_t)(uint32_t)i * m) >> 32);
+    const int r = r0 + (int)rr, q = q0 + i - (int)rr * nq, cb = q * E;
+    const uint32_t sa = sbase + (uint32_t)((r * L::ROW + L::swz(q) * E) * (int)sizeof(T));
+    const T* src = g + (int64_t)(gy0 + r) * pitch + gx0 + cb;
+    if (vec && cb >= c0 && cb + E <= c1) {
+      cp_async16(sa, src);
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (cb + e >= c0 && cb + e < c1) cp_async(sa + (uint32_t)(e * sizeof(T)), src + e);
+    }
+  }
+}
+
+// Halo refresh, warp-specialised: the ring is cut into 16 tasks (N, S, the 4
+// corners, and the W and E side columns in 5 row slices each), each owned by
+// one neighbour; a warp polls that neighbour's epoch flag and streams the
+// task's cells in with cp.async as soon as they are published, so the waits
+// and loads overlap across warps.
 template <typename T, int K>
 __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restrict__ g,
                                                      int64_t pitch, int gx0, int gy0,
@@ -248,45 +280,46 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
                                                      int tx, int ty, int ry0, int oy0, int oy1,
                                                      int ry1, int rx0, int ox0, int ox1, int rx1) {
   typedef Tile<T, K> L;
+#ifndef DTB_SIDE_PARTS
+#define DTB_SIDE_PARTS 1
+#endif
+  constexpr int kSideParts = DTB_SIDE_PARTS;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int k = warp; k < 8; k += nw) {
+  const bool vec = ((gx0 % L::EPC) == 0) && ((pitch % L::EPC) == 0);
+  const int side_rows = oy1 - oy0;
+  int polled = -1;  // neighbour this warp last waited for
+  for (int k = warp; k < 6 + 2 * kSideParts; k += nw) {
     int dx, dy, r0, r1, c0, c1;
-    switch (k) {
-      case 0: dx = 0; dy = -1; r0 = ry0; r1 = oy0; c0 = ox0; c1 = ox1; break;
-      case 1: dx = 0; dy = 1; r0 = oy1; r1 = ry1; c0 = ox0; c1 = ox1; break;
-      case 2: dx = -1; dy = 0; r0 = oy0; r1 = oy1; c0 = rx0; c1 = ox0; break;
-      case 3: dx = 1; dy = 0; r0 = oy0; r1 = oy1; c0 = ox1; c1 = rx1; break;
-      case 4: dx = -1; dy = -1; r0 = ry0; r1 = oy0; c0 = rx0; c1 = ox0; break;
-      case 5: dx = 1; dy = -1; r0 = ry0; r1 = oy0; c0 = ox1; c1 = rx1; break;
-      case 6: dx = -1; dy = 1; r0 = oy1; r1 = ry1; c0 = rx0; c1 = ox0; break;
-      default: dx = 1; dy = 1; r0 = oy1; r1 = ry1; c0 = ox1; c1 = rx1; break;
+    if (k < 6) {
+      switch (k) {
+        case 0: dx = 0; dy = -1; r0 = ry0; r1 = oy0; c0 = ox0; c1 = ox1; break;
+        case 1: dx = 0; dy = 1; r0 = oy1; r1 = ry1; c0 = ox0; c1 = ox1; break;
+        case 2: dx = -1; dy = -1; r0 = ry0; r1 = oy0; c0 = rx0; c1 = ox0; break;
+        case 3: dx = 1; dy = -1; r0 = ry0; r1 = oy0; c0 = ox1; c1 = rx1; break;
+        case 4: dx = -1; dy = 1; r0 = oy1; r1 = ry1; c0 = rx0; c1 = ox0; break;
+        default: dx = 1; dy = 1; r0 = oy1; r1 = ry1; c0 = ox1; c1 = rx1; break;
+      }
+    } else {
+      const int j = (k - 6) % kSideParts;
+      const bool west = (k - 6) < kSideParts;
+      dx = west ? -1 : 1;
+      dy = 0;
+      r0 = oy0 + side_rows * j / kSideParts;
+      r1 = oy0 + side_rows * (j + 1) / kSideParts;
+      c0 = west ? rx0 : ox1;
+      c1 = west ? ox0 : rx1;
     }
     const int nxt = tx + dx, nyt = ty + dy;
     if (r1 <= r0 || c1 <= c0 || nxt < 0 || nxt >= ntx || nyt < 0 || nyt >= nty) continue;
-    if (lane == 0) {
-      const int* f = flags + nyt * ntx + nxt;
-      while (ld_acquire_gpu(f) < epoch) __nanosleep(32);
+    const int nb = nyt * ntx + nxt;
+    if (nb != polled) {
+      if (lane == 0)
+        while (ld_acquire_gpu(flags + nb) < epoch) __nanosleep(32);
+      __syncwarp();
+      polled = nb;
     }
-    __syncwarp();
-    if (c1 - c0 >= 16) {  // wide region: lanes across columns
-      for (int r = r0; r < r1; ++r) {
-        const T* src = g + (int64_t)(gy0 + r) * pitch + gx0;
-        const uint32_t srow = sbase + (uint32_t)(r * L::ROW * (int)sizeof(T));
-        for (int c = c0 + lane; c < c1; c += 32)
-          cp_async(srow + (uint32_t)((L::swz(c / L::EPC) * L::EPC + c % L::EPC) * (int)sizeof(T)),
-                   src + c);
-      }
-    } else {  // narrow region: flattened, column-fastest (few sectors per warp load)
-      const int w = c1 - c0, n = (r1 - r0) * w;
-      const uint32_t m = (65535u + w) / w;
-      for (int i = lane; i < n; i += 32) {
-        const uint32_t q = ((uint32_t)i * m) >> 16;
-        const int r = r0 + (int)q, c = c0 + i - (int)q * w;
-        cp_async(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)),
-                 g + (int64_t)(gy0 + r) * pitch + gx0 + c);
-      }
-    }
+    warp_g2s_chunks<T, K>(sbase, g, pitch, gx0, gy0, r0, r1, c0, c1, vec, lane);
   }
   cp_async_wait_all();
 }
