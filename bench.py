@@ -295,7 +295,7 @@ def run_b200(args):
     elem = 8 if dtype == "f64" else 4
     w = StencilWeights.diffusive(0.2)
     dev = torch.device("cuda", local)
-    a = torch.empty((ny + 2, nx + 2), dtype=tdt, device=dev)
+    a = torch.empty((ny + 2, (nx + 2 + 31) // 32 * 32), dtype=tdt, device=dev)  # 128-B pitch
     b = torch.empty_like(a)
     fill_random_device(a, nx, ny, 1, ghost=0.0)
     plan = plan_b200(nx, ny, elem, steps, 1)
@@ -340,7 +340,7 @@ def run_b200(args):
     e2e = None
     if rank == 0:
         host_in = torch.empty((ny + 2, nx + 2), dtype=tdt, pin_memory=True)
-        host_in.copy_(a.cpu())
+        host_in.copy_(a[:, :nx + 2].cpu())
         host_out = torch.empty_like(host_in).pin_memory()
         import ctypes
         lib = _native.lib()

@@ -427,9 +427,17 @@ template <typename T, int K, int NW, bool DYN>
 __global__ void __launch_bounds__(NW * 32, 1)
 stream_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int nx, int ny,
               Weights<T> wt, int steps, int poison, int nbuf, int buf_elems,
-              const __grid_constant__ Geometry geo) {
+              unsigned long long* __restrict__ trace, const __grid_constant__ Geometry geo) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* bufs[2] = {reinterpret_cast<T*>(smem_raw), reinterpret_cast<T*>(smem_raw) + buf_elems};
+  const bool tracing = trace != nullptr && threadIdx.x == 0;
+  unsigned long long t_wait = 0, t_comp = 0, t_store = 0, tc = tracing ? clock64() : 0;
+#define DTB_MARK(acc)                                  \
+  if (tracing) {                                       \
+    const unsigned long long now_ = clock64();         \
+    acc += now_ - tc;                                  \
+    tc = now_;                                         \
+  }
   const int ntiles = geo.ntx * geo.nty;
   auto issue_load = [&](int t, T* tile) {
     const int tx = t % geo.ntx, ty = t / geo.ntx;
@@ -451,19 +459,27 @@ stream_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int
       cp_async_wait_all();
     }
     __syncthreads();
+    DTB_MARK(t_wait)
     const int tx = t % geo.ntx, ty = t / geo.ntx;
     const int4 cx = geo.col[tx], cy = geo.row[ty];
     const int Lw = cx.w - cx.z, Lh = cy.w - cy.z;
     advance<T, K, DYN>(tile, Lw, Lh, steps, wt, poison != 0, cx.z > -1, cx.w < nx + 1,
                        cy.z > -1, cy.w < ny + 1);
+    DTB_MARK(t_comp)
     // owned cells, plus the ghost ring where the tile touches the domain edge
     const int sx0 = cx.x - (cx.x == 0), sx1 = cx.y + (cx.y == nx);
     const int sy0 = cy.x - (cy.x == 0), sy1 = cy.y + (cy.y == ny);
     s2g_rows<T, K>(tile, dst, pitch, cx.z + 1, cy.z + 1, sy0 - cy.z, sy1 - cy.z, sx0 - cx.z,
                    sx1 - cx.z);
     __syncthreads();  // every read of this buffer is done before it is refilled
+    DTB_MARK(t_store)
   }
   cp_async_wait_all();
+#undef DTB_MARK
+  if (tracing) {
+    unsigned long long* tr = trace + 8 * blockIdx.x;
+    tr[0] += t_comp; tr[1] += t_store; tr[2] += t_wait; tr[4] += i;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -834,15 +850,29 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
   int64_t done = 0;
   const int nbuf = p.ctas_per_sm;  // the planner's occupancy 2 == double-buffered CTA
   const int buf_elems = (int)(p.smem_bytes / (int64_t)sizeof(T));
+  unsigned long long* strace = nullptr;
+  const size_t strace_bytes = (size_t)p.ctas * 8 * sizeof(unsigned long long);
+  if (tracing) {
+    CUDA_TRY(cudaMallocAsync((void**)&strace, strace_bytes, st));
+    CUDA_TRY(cudaMemsetAsync(strace, 0, strace_bytes, st));
+  }
   for (int64_t i = 0; i < passes; ++i) {
     const int s = (int)std::min<int64_t>(p.h, steps - done);
     T* dst = ((passes - 1 - i) % 2 == 0) ? d_out : tmp;
     kern<<<p.ctas, threads, (size_t)smem * nbuf, st>>>(src, dst, pitch, nx, ny, wt, s,
-                                                       poison ? 1 : 0, nbuf, buf_elems, geo);
+                                                       poison ? 1 : 0, nbuf, buf_elems, strace,
+                                                       geo);
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
     src = dst;
     done += s;
+  }
+  if (tracing) {
+    std::vector<unsigned long long> h_tr((size_t)p.ctas * 8);
+    CUDA_TRY(cudaMemcpyAsync(h_tr.data(), strace, strace_bytes, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    CUDA_TRY(cudaFreeAsync(strace, st));
+    g_trace.assign(h_tr.begin(), h_tr.end());
   }
   return DTB_OK;
 }
@@ -1021,7 +1051,9 @@ int solve_host(const T* in, T* out, int64_t nx, int64_t ny, int64_t pitch, const
   if (rc) return rc;
   int device;
   CUDA_TRY(cudaGetDevice(&device));
-  const size_t bytes = (size_t)(ny + 2) * pitch * sizeof(T);
+  // device copy with a 128-byte-multiple pitch: 16-byte aligned tile copies
+  const int64_t dpitch = (nx + 2 + 31) / 32 * 32;
+  const size_t bytes = (size_t)(ny + 2) * dpitch * sizeof(T);
   void* io = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -1031,10 +1063,13 @@ int solve_host(const T* in, T* out, int64_t nx, int64_t ny, int64_t pitch, const
   T* d_in = reinterpret_cast<T*>(io);
   T* d_out = reinterpret_cast<T*>(reinterpret_cast<char*>(io) + bytes);
   cudaStream_t st = 0;
-  CUDA_TRY(cudaMemcpyAsync(d_in, in, bytes, cudaMemcpyHostToDevice, st));
-  rc = solve_dev<T>(d_in, d_out, nx, ny, pitch, w, total_steps, t_depth, valid, flags, st, rep);
+  const size_t row = (size_t)(nx + 2) * sizeof(T);
+  CUDA_TRY(cudaMemcpy2DAsync(d_in, dpitch * sizeof(T), in, pitch * sizeof(T), row, ny + 2,
+                             cudaMemcpyHostToDevice, st));
+  rc = solve_dev<T>(d_in, d_out, nx, ny, dpitch, w, total_steps, t_depth, valid, flags, st, rep);
   if (rc) return rc;
-  CUDA_TRY(cudaMemcpyAsync(out, d_out, bytes, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpy2DAsync(out, pitch * sizeof(T), d_out, dpitch * sizeof(T), row, ny + 2,
+                             cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   return DTB_OK;
 }

@@ -8,7 +8,8 @@
 
 namespace dtb {
 
-bool make_split(int N, int n, int h, int align, int maxL, int min_owned, Split& s, int off) {
+bool make_split(int N, int n, int h, int align, int maxL, int min_owned, Split& s, int off,
+                int start_align) {
   s = Split();
   if (n < 1 || N < 1) return false;
   s.n = n;
@@ -31,6 +32,20 @@ bool make_split(int N, int n, int h, int align, int maxL, int min_owned, Split& 
     x += (int)own;
   }
   if (x != N) return false;
+  if (start_align > 1) {
+    // move interior boundaries so each load region starts on a 16-byte chunk
+    // of the padded row (padded index l0 + 1 = o0 - h + 1 divisible):
+    // whole-chunk cp.async / vector stores for the tile copies
+    for (int i = 1; i < n; ++i) {
+      const int b = s.o0[i];
+      const int r = ((b - h + 1) % start_align + start_align) % start_align;
+      const int nb = (r * 2 <= start_align) ? b - r : b + (start_align - r);
+      if (nb - s.o0[i - 1] >= std::max(1, min_owned) && s.o1[i] - nb >= std::max(1, min_owned)) {
+        s.o1[i - 1] = nb;
+        s.o0[i] = nb;
+      }
+    }
+  }
   for (int i = 0; i < n; ++i) {
     s.l0[i] = std::max(s.o0[i] - left[i], -1);
     s.l1[i] = std::min(s.o1[i] + right[i], N + 1);
@@ -159,7 +174,7 @@ bool plan_resident(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInf
       const int ntx_min = (int)((nx + 2 + Lw_max - 1) / Lw_max);
       for (int ntx = std::max(1, ntx_min); ntx <= std::min<int64_t>(dev.sms, nx); ++ntx) {
         Split sx;
-        if (!make_split((int)nx, ntx, h, K, Lw_max, ntx > 1 ? h : 1, sx)) continue;
+        if (!make_split((int)nx, ntx, h, K, Lw_max, ntx > 1 ? h : 1, sx, 0, 16 / elem)) continue;
         const int nty_max = (int)std::min<int64_t>(dev.sms / ntx, ny);
         for (int nty = nty_max; nty >= std::max(1, nty_max - 2); --nty) {
           Split sy;
@@ -215,7 +230,7 @@ bool plan_streaming(int64_t nx, int64_t ny, int elem, int64_t steps, const DevIn
             (nx + 2 + Lw_max - 1) / Lw_max, (nx + per - 1) / per - 1));
         for (int ntx = ntx_min; ntx <= ntx_min + 3 && ntx <= nx; ++ntx) {
           Split sx;
-          if (!make_split((int)nx, ntx, h, K, Lw_max, 1, sx)) continue;
+          if (!make_split((int)nx, ntx, h, K, Lw_max, 1, sx, 0, 16 / elem)) continue;
           // tallest tiles that fit, and a few shorter ones (band balance)
           const int per_y = std::max(1, maxRows - 2 * h);
           int nty0 = (int)std::max<int64_t>(

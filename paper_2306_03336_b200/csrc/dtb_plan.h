@@ -62,8 +62,10 @@ struct Plan {
 // load extent exceeds maxL or a tile owns fewer than min_owned cells.
 // `align`/`off`: load extents are grown (when the neighbour has the cells)
 // to L = off (mod align); a miss is allowed in y (off != 0), flagged dyn in x.
+// `start_align` > 1: interior boundaries are nudged so every load region
+// starts at a padded index divisible by it (16-byte aligned tile copies).
 bool make_split(int N, int n, int h, int align, int maxL, int min_owned, Split& s,
-                int off = 0);
+                int off = 0, int start_align = 1);
 
 // Choose the execution plan. force: 0 auto, 1 streaming, 2 naive.
 // depth > 0 pins the halo depth.

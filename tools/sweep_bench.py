@@ -8,7 +8,7 @@ from paper_2306_03336_b200.prng import fill_random_device
 
 def timeit(nx, ny, steps, dtype, flags=0, depth=None, reps=3):
     tdt = torch.float64 if dtype == "f64" else torch.float32
-    a = torch.empty((ny + 2, nx + 2), dtype=tdt, device="cuda"); b = torch.empty_like(a)
+    a = torch.empty((ny + 2, (nx + 2 + 31) // 32 * 32), dtype=tdt, device="cuda"); b = torch.empty_like(a)
     fill_random_device(a, nx, ny, 1)
     w = StencilWeights.diffusive(0.2)
     j2d5pt_device(a, b, nx, ny, w, steps, flags=flags, depth=depth)
@@ -31,10 +31,26 @@ if __name__ == "__main__":
                       flags | (_native.FLAG_FORCE_DEPTH if depth else 0))
         ms = timeit(nx, ny, steps, dtype, flags, depth)
         extra = {}
+        if os.environ.get("DTB_TRACE") and p.mode == "streaming":
+            import ctypes
+            tdt = torch.float64 if dtype == "f64" else torch.float32
+            a = torch.empty((ny + 2, (nx + 2 + 31) // 32 * 32), dtype=tdt, device="cuda"); b = torch.empty_like(a)
+            fill_random_device(a, nx, ny, 1)
+            j2d5pt_device(a, b, nx, ny, StencilWeights.diffusive(0.2), steps,
+                          flags=flags | _native.FLAG_TRACE, depth=depth)
+            torch.cuda.synchronize()
+            buf = (ctypes.c_int64 * (8 * 200))()
+            n = _native.lib().dtb_last_trace(buf, 8 * 200)
+            v = [list(buf[8 * i:8 * i + 8]) for i in range(n)]
+            tot = [sum(x[k] for x in v) / max(n, 1) for k in range(8)]
+            cyc = tot[0] + tot[1] + tot[2]
+            extra = {"stream_frac": {"compute": round(tot[0] / cyc, 3), "store": round(tot[1] / cyc, 3),
+                                     "load_wait": round(tot[2] / cyc, 3)},
+                     "tiles_per_cta": round(tot[4], 1), "cycles_per_tile": round(cyc / max(tot[4], 1))}
         if os.environ.get("DTB_TRACE") and p.mode == "resident":
             import ctypes
             tdt = torch.float64 if dtype == "f64" else torch.float32
-            a = torch.empty((ny + 2, nx + 2), dtype=tdt, device="cuda"); b = torch.empty_like(a)
+            a = torch.empty((ny + 2, (nx + 2 + 31) // 32 * 32), dtype=tdt, device="cuda"); b = torch.empty_like(a)
             fill_random_device(a, nx, ny, 1)
             j2d5pt_device(a, b, nx, ny, StencilWeights.diffusive(0.2), steps,
                           flags=flags | _native.FLAG_TRACE, depth=depth)
