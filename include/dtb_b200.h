@@ -48,6 +48,8 @@ extern "C" {
 #define DTB_FLAG_FORCE_NAIVE 4u     /* one global-memory step per launch (the T=1 HBM baseline) */
 #define DTB_FLAG_FORCE_DEPTH 8u     /* use t_depth as the temporal halo depth instead of the planner's */
 #define DTB_FLAG_TRACE 16u          /* resident kernel: per-CTA clock64 phase counters (dtb_last_trace) */
+#define DTB_FLAG_FORCE_PIPE 32u     /* use the pipelined (warp-pipeline, column-strip) streaming kernel */
+#define DTB_FLAG_FORCE_RESIDENT 64u /* use the smem-resident kernel (fails if the grid does not fit) */
 
 /* Half-open rectangle in interior coordinates (grid.py:38-92). */
 typedef struct dtb_rect {
@@ -67,7 +69,8 @@ typedef struct dtb_report {
 
 /* The B200 plan (what plan_device_tiles' TilingPlan is for the reference). */
 typedef struct dtb_plan_info {
-  int32_t mode;         /* 0 resident (persistent, smem-resident), 1 streaming, 2 naive */
+  int32_t mode;         /* 0 resident (persistent, smem-resident), 1 streaming (tile sweep),
+                           2 naive, 3 pipelined streaming (warp pipeline) */
   int32_t elem_bytes;
   int32_t lane_elems;   /* K: consecutive columns per lane */
   int32_t warps;        /* warps per CTA (row bands) */

@@ -26,6 +26,8 @@ FLAG_FORCE_STREAM = 2
 FLAG_FORCE_NAIVE = 4
 FLAG_FORCE_DEPTH = 8
 FLAG_TRACE = 16
+FLAG_FORCE_PIPE = 32
+FLAG_FORCE_RESIDENT = 64
 
 
 class DtbRect(ctypes.Structure):

@@ -26,6 +26,7 @@
 
 #include "../../include/dtb_b200.h"
 #include "dtb_core.cuh"
+#include "dtb_pipe.cuh"
 #include "dtb_plan.h"
 
 namespace dtb {
@@ -483,6 +484,63 @@ stream_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int
 }
 
 // ---------------------------------------------------------------------------
+// pipelined streaming pass (dtb_pipe.cuh): NW/S pipelines of S warps per CTA,
+// each pipeline marching column-strip segments; h = 2S steps per pass.
+// ---------------------------------------------------------------------------
+template <int S>
+struct PipeSmem {
+  int prod[S], cons[S];
+};
+
+template <typename T, int K, int NW, int S, bool DYN>
+__global__ void __launch_bounds__(NW * 32, 1)
+pipe_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int nx, int ny,
+            Weights<T> wt, int steps, const __grid_constant__ Geometry geo) {
+  constexpr int P = NW / S;
+  typedef Tile<T, K> L;
+  constexpr int RB = L::ROW * (int)sizeof(T);
+  constexpr int kRing0Rows = PipeCfg<NW>::kRing0Rows, kRingRows = PipeCfg<NW>::kRingRows;
+  constexpr int kPipeBytes = (kRing0Rows + (S - 1) * kRingRows) * RB;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, p = warp / S, s = warp % S;
+  PipeSmem<S>* ctl = reinterpret_cast<PipeSmem<S>*>(smem_raw + P * kPipeBytes);
+  if (threadIdx.x < P * S) {
+    ctl[threadIdx.x / S].prod[threadIdx.x % S] = 0;
+    ctl[threadIdx.x / S].cons[threadIdx.x % S] = 0;
+  }
+  __syncthreads();
+  const uint32_t pbase = (uint32_t)__cvta_generic_to_shared(smem_raw + p * kPipeBytes);
+  // ring s (s >= 1) follows ring0
+  const uint32_t ring_in = s == 0 ? pbase : pbase + (uint32_t)(kRing0Rows + (s - 1) * kRingRows) * RB;
+  const uint32_t ring_out = pbase + (uint32_t)(kRing0Rows + s * kRingRows) * RB;
+  const int levels = max(0, min(2, steps - 2 * s));
+  LaneCtx lc;
+  lc.lane = threadIdx.x & 31;
+  lc.first = lc.lane == 0;
+  const int ntiles = geo.ntx * geo.nty;
+  int seq = 0;
+  for (int t = blockIdx.x * P + p; t < ntiles; t += gridDim.x * P) {
+    const int tx = t % geo.ntx, ty = t / geo.ntx;
+    const int4 cx = geo.col[tx], cy = geo.row[ty];
+    PipeTile pt;
+    pt.Lw = cx.w - cx.z;
+    pt.Lh = cy.w - cy.z;
+    pt.gx0 = cx.z + 1;
+    pt.gy0 = cy.z + 1;
+    pt.ox0 = cx.x - (cx.x == 0) - cx.z;
+    pt.ox1 = cx.y + (cx.y == nx) - cx.z;
+    pt.oy0 = cy.x - (cy.x == 0) - cy.z;
+    pt.oy1 = cy.y + (cy.y == ny) - cy.z;
+    pt.vec = ((pt.gx0 % L::EPC) == 0) && ((pitch % L::EPC) == 0);
+    lc.last = lc.lane == (pt.Lw - 1) / K;
+    lc.last_e = (pt.Lw - 1) % K;
+    pipe_stage<T, K, NW, DYN>(pt, s, S, levels, seq, src, dst, pitch, ring_in, ring_out,
+                          ctl[p].prod, ctl[p].cons, wt, lc);
+    seq += pt.Lh;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // resident: persistent cooperative kernel, neighbour-flag halo exchange
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void st_release(int* p, int v) {
@@ -833,6 +891,7 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
     }
     return DTB_OK;
   }
+  if (p.mode == 3) return DTB_EINFEASIBLE;  // handled by launch_pipe
   // streaming passes, ping-ponging dst between out and a scratch grid
   auto kern = stream_kernel<T, K, NW, DYN>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -877,6 +936,46 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
   return DTB_OK;
 }
 
+// pipelined streaming passes of h = 2S steps (mode 3), PW warps per CTA
+template <typename T, int K, int PW, bool DYN>
+int launch_pipe(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch,
+                int nx, int ny, const Weights<T>& wt, int64_t steps, cudaStream_t st) {
+  constexpr int S = 4, P = PW / S;
+  auto kern = pipe_kernel<T, K, PW, S, DYN>;
+  const int pipe_bytes = (PipeCfg<PW>::kRing0Rows + (S - 1) * PipeCfg<PW>::kRingRows) *
+                         Tile<T, K>::ROW * (int)sizeof(T);
+  const int psmem = P * pipe_bytes + (int)sizeof(PipeSmem<S>) * P;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem));
+  int device;
+  CUDA_TRY(cudaGetDevice(&device));
+  const size_t grid_bytes = (size_t)(ny + 2) * pitch * sizeof(T);
+  const int64_t passes = (steps + 2 * S - 1) / (2 * S);
+  T* tmp = nullptr;
+  if (passes > 1) {
+    void* scratch = nullptr;
+    std::lock_guard<std::mutex> lk(g_mu);
+    int rc = arena_get(g_scratch[device & 15], grid_bytes, &scratch);
+    if (rc) return rc;
+    tmp = reinterpret_cast<T*>(scratch);
+  }
+  const int64_t ntiles = (int64_t)geo.ntx * geo.nty;
+  int sms = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  const int ctas = (int)std::min<int64_t>(sms, (ntiles + P - 1) / P);
+  const T* src = d_in;
+  int64_t done = 0;
+  for (int64_t i = 0; i < passes; ++i) {
+    const int s = (int)std::min<int64_t>(2 * S, steps - done);
+    T* dst = ((passes - 1 - i) % 2 == 0) ? d_out : tmp;
+    kern<<<ctas, PW * 32, psmem, st>>>(src, dst, pitch, nx, ny, wt, s, geo);
+    g_launches += 1;
+    CUDA_TRY(cudaGetLastError());
+    src = dst;
+    done += s;
+  }
+  return DTB_OK;
+}
+
 template <typename T, int K, int NW>
 int dispatch_dyn(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch,
                  int nx, int ny, const Weights<T>& wt, int64_t steps, bool poison,
@@ -889,6 +988,14 @@ int dispatch_dyn(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, in
 template <typename T>
 int dispatch(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch, int nx,
              int ny, const Weights<T>& wt, int64_t steps, bool poison, cudaStream_t st) {
+  if (p.mode == 3) {
+#ifndef DTB_PIPE_WARPS
+#define DTB_PIPE_WARPS 16
+#endif
+    constexpr int KK = sizeof(T) == 8 ? 4 : 8;
+    return p.dyn() ? launch_pipe<T, KK, DTB_PIPE_WARPS, true>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, st)
+                   : launch_pipe<T, KK, DTB_PIPE_WARPS, false>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, st);
+  }
 #define DTB_SHAPE(KK, WW)                                                                  \
   if (p.K == KK && p.warps == WW)                                                          \
     return dispatch_dyn<T, KK, WW>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st);
@@ -994,7 +1101,8 @@ int solve_dev(const T* d_in, T* d_out, int64_t nx, int64_t ny, int64_t pitch, co
   DevInfo dev;
   rc = query_dev(dev);
   if (rc) return rc;
-  int force = (flags & DTB_FLAG_FORCE_NAIVE) ? 2 : (flags & DTB_FLAG_FORCE_STREAM) ? 1 : 0;
+  int force = (flags & DTB_FLAG_FORCE_NAIVE) ? 2 : (flags & DTB_FLAG_FORCE_STREAM) ? 1
+              : (flags & DTB_FLAG_FORCE_PIPE) ? 3 : (flags & DTB_FLAG_FORCE_RESIDENT) ? 4 : 0;
   int depth = (flags & DTB_FLAG_FORCE_DEPTH) ? (int)t_depth : 0;
   Plan p;
   char err[512];
@@ -1127,7 +1235,8 @@ int dtb_plan(int64_t nx, int64_t ny, int32_t elem_bytes, int64_t total_steps, in
   } else {
     cudaGetLastError();  // no GPU: plan for the B200 defaults (148 SMs, 227 KB)
   }
-  int force = (flags & DTB_FLAG_FORCE_NAIVE) ? 2 : (flags & DTB_FLAG_FORCE_STREAM) ? 1 : 0;
+  int force = (flags & DTB_FLAG_FORCE_NAIVE) ? 2 : (flags & DTB_FLAG_FORCE_STREAM) ? 1
+              : (flags & DTB_FLAG_FORCE_PIPE) ? 3 : (flags & DTB_FLAG_FORCE_RESIDENT) ? 4 : 0;
   int depth = (flags & DTB_FLAG_FORCE_DEPTH) ? (int)t_depth : 0;
   Plan p;
   char err[512];

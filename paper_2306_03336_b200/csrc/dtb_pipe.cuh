@@ -1,0 +1,284 @@
+// dtb_pipe.cuh — the pipelined (2.5-D) streaming kernel.
+//
+// Temporal blocking by a warp pipeline instead of a tile-wide sweep: a
+// "pipeline" is S warps; warp s advances rows from time level 2s to 2s+2 and
+// hands them to warp s+1 through a small shared-memory ring, so the h = 2S
+// fused steps of a pass flow through the pipeline while it marches down a
+// tall column strip ("segment") of the domain:
+//
+//   HBM --cp.async--> ring0 -> [warp 0: t -> t+2] -> ring1 -> [warp 1] -> ...
+//                              -> [warp S-1: t+h-2 -> t+h] --STG--> HBM
+//
+// Compared with the tile sweep (dtb_core.cuh) there are no band seams, no
+// CTA-wide barriers and no pre-read halo registers; y-redundancy exists only
+// at segment ends (segments are hundreds to thousands of rows) and the HBM
+// traffic of a pass is one read + one write of every owned cell, overlapped
+// with the FP work by the ring prefetch. Each warp spans the strip width
+// (32*K columns, lane-owned K-column chunks, shuffles for W/E) exactly as in
+// the tile sweep; every update is the same FMA-free W,E,S,C,N expression
+// (kernel.py:137-139), so results stay bitwise equal to jacobi_reference.
+//
+// Synchronisation inside a pipeline is by monotonic row counters in shared
+// memory (st.release.cta / ld.acquire.cta): prod[s] = rows written into ring
+// s, cons[s] = rows ring s's reader no longer needs.
+#pragma once
+#include "dtb_core.cuh"
+
+namespace dtb {
+
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];"
+               : "=r"(v)
+               : "r"((uint32_t)__cvta_generic_to_shared(p))
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)),
+               "r"(v)
+               : "memory");
+}
+__device__ __forceinline__ void pipe_cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void pipe_cp_async(uint32_t dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void pipe_cp_async(uint32_t dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void pipe_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void pipe_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
+// Ring geometry (rows of 32*K elements, the tile row layout incl. swizzle),
+// per CTA width: 8 warps = 2 pipelines with deep rings, 16 warps = 4
+// pipelines with shallower rings (the smem budget). Block-level flow control
+// needs kRingRows >= 12 to stay deadlock-free (see pipe_stage).
+template <int NW>
+struct PipeCfg {
+  static constexpr int kRing0Rows = NW >= 16 ? 12 : 16;  // warp 0's HBM prefetch ring
+  static constexpr int kRingRows = NW >= 16 ? 12 : 16;   // ring between consecutive warps
+  static constexpr int kPrefetch = NW >= 16 ? 6 : 8;     // HBM prefetch rows in flight
+};
+
+struct PipeTile {
+  int Lw, Lh;        // load region (tile-local rows/cols)
+  int gx0, gy0;      // padded global coords of tile (0,0)
+  int ox0, ox1;      // store columns (owned, + ghost at domain edges), tile-local
+  int oy0, oy1;      // store rows, tile-local
+  bool vec;          // global side 16-byte aligned per chunk
+};
+
+// One pipeline stage warp advancing one tile by `levels` (0, 1 or 2) steps.
+// seq0: the pipeline-wide row sequence number of this tile's row 0 (ring
+// slot = seq % ring rows). `src` is read only by stage 0; `dst` written only
+// by the last stage.
+template <typename T, int K, int NW, bool DYN>
+__device__ __forceinline__ void pipe_stage(const PipeTile& pt, int stage, int nstages, int levels,
+                                           int seq0, const T* __restrict__ src,
+                                           T* __restrict__ dst, int64_t pitch, uint32_t ring_in,
+                                           uint32_t ring_out, int* prod, int* cons,
+                                           const Weights<T>& wt, const LaneCtx& lc) {
+  typedef Tile<T, K> L;
+  constexpr int E = L::EPC, CH = L::CH;
+  constexpr uint32_t RB = (uint32_t)(L::ROW * sizeof(T));  // bytes per ring row
+  const int lane = lc.lane;
+  const int Lh = pt.Lh;
+  uint32_t off[CH];
+#pragma unroll
+  for (int j = 0; j < CH; ++j) off[j] = (uint32_t)(L::swz(lane * CH + j) * 16);
+  const bool first = stage == 0, lastst = stage == nstages - 1;
+  constexpr int kRing0Rows = PipeCfg<NW>::kRing0Rows, kRingRows = PipeCfg<NW>::kRingRows,
+                kPrefetch = PipeCfg<NW>::kPrefetch;
+
+  // ---- input rows --------------------------------------------------------
+  // stage 0: the warp prefetches its own lanes' chunks of row q into ring0
+  auto issue_row = [&](int q) {
+    if (q < Lh) {
+      const uint32_t srow = ring_in + (uint32_t)((seq0 + q) % kRing0Rows) * RB;
+      const T* g = src + (int64_t)(pt.gy0 + q) * pitch + pt.gx0;
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        const int cb = (lane * CH + j) * E;
+        if (pt.vec && cb + E <= pt.Lw) {
+          pipe_cp_async16(srow + off[j], g + cb);
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e)
+            if (cb + e < pt.Lw) pipe_cp_async(srow + off[j] + (uint32_t)(e * sizeof(T)), g + cb + e);
+        }
+      }
+    }
+    pipe_commit();
+  };
+  // block-level flow control (steady loop): wait until rows [.., q_hi] are in
+  // the input ring / ring slots up to output row q_hi are free
+  auto wait_in = [&](int q_hi) {
+    if (!first) {
+      if (lane == 0)
+        while (ld_acquire_cta(prod + stage) < seq0 + q_hi + 1) __nanosleep(20);
+      __syncwarp();
+    }
+  };
+  auto release_in = [&](int q_done) {  // input rows < q_done fully read
+    if (!first) {
+      __syncwarp();
+      if (lane == 0) st_release_cta(cons + stage, seq0 + q_done);
+    }
+  };
+  auto wait_out = [&](int q_hi) {
+    if (!lastst) {
+      if (lane == 0)
+        while (ld_acquire_cta(cons + stage + 1) < seq0 + q_hi - kRingRows + 1) __nanosleep(20);
+      __syncwarp();
+    }
+  };
+  auto release_out = [&](int q_done) {  // output rows < q_done written
+    if (!lastst) {
+      __syncwarp();
+      if (lane == 0) st_release_cta(prod + stage + 1, seq0 + q_done);
+    }
+  };
+  auto get_row_nosync = [&](int q, T (&v)[K]) {
+    if (first) {
+      issue_row(q + kPrefetch);
+      pipe_wait_group<kPrefetch>();  // row q's group has landed (this lane's chunks)
+      load_row_at<CH>(ring_in + (uint32_t)((seq0 + q) % kRing0Rows) * RB, off, v);
+    } else {
+      load_row_at<CH>(ring_in + (uint32_t)((seq0 + q) % kRingRows) * RB, off, v);
+    }
+  };
+  auto get_row = [&](int q, T (&v)[K]) {
+    wait_in(q);
+    get_row_nosync(q, v);
+    // rows up to q-2 are in registers and no longer read from the ring
+    if (q >= 2) release_in(q - 1);
+  };
+  // ---- output rows -------------------------------------------------------
+  const int c_lo = lane * K;
+  const bool full_vec = pt.vec && c_lo >= pt.ox0 && c_lo + K <= pt.ox1;
+  auto put_row_nosync = [&](int q, const T (&v)[K]) {
+    if (lastst) {
+      if (q >= pt.oy0 && q < pt.oy1) {
+        T* g = dst + (int64_t)(pt.gy0 + q) * pitch + pt.gx0 + c_lo;
+        if (full_vec) {
+          typedef typename Arith<T>::vec_t V;
+#pragma unroll
+          for (int j = 0; j < CH; ++j) {
+            V x;
+            T* px = reinterpret_cast<T*>(&x);
+#pragma unroll
+            for (int e = 0; e < E; ++e) px[e] = v[j * E + e];
+            *reinterpret_cast<V*>(g + j * E) = x;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < K; ++e)
+            if (c_lo + e >= pt.ox0 && c_lo + e < pt.ox1) g[e] = v[e];
+        }
+      }
+    } else {
+      store_row_at<CH>(ring_out + (uint32_t)((seq0 + q) % kRingRows) * RB, off, v);
+    }
+  };
+  auto put_row = [&](int q, const T (&v)[K]) {
+    wait_out(q);
+    put_row_nosync(q, v);
+    release_out(q + 1);
+  };
+
+  if (first) {
+    for (int q = 0; q < kPrefetch; ++q) issue_row(q);
+  }
+
+  if (levels == 0) {
+    for (int q = 0; q < Lh; ++q) {
+      T v[K];
+      get_row(q, v);
+      put_row(q, v);
+    }
+  } else if (levels == 1) {
+    T a0[K], a1[K], a2[K], o[K];
+    get_row(0, a1);
+    put_row(0, a1);  // frozen row
+    if (Lh > 1) get_row(1, a2);
+    for (int q = 1; q + 1 < Lh; ++q) {
+      copy_row<T, K>(a1, a0);
+      copy_row<T, K>(a2, a1);
+      get_row(q + 1, a2);
+      row_update<T, K, DYN>(a0, a1, a2, o, wt, lc);
+      put_row(q, o);
+    }
+    if (Lh > 1) put_row(Lh - 1, a2);  // frozen row
+  } else {
+    // two levels, skewed: iteration r loads t(r+2), computes b(r) = L1(t) and
+    // out(r-2) = L2(b); t(q) in T[q%4], b(q) in B[q%4] (static after unroll)
+    T t0[K], t1[K], t2[K], t3[K], b0[K], b1[K], b2[K], b3[K], o[K];
+    get_row(0, t0);
+    if (Lh > 1) get_row(1, t1);
+#define DTB_PIPE_ITER(TM1, TC, TP1, TP2, BR, BM1, BM2, BM3)                       \
+  {                                                                               \
+    if (r + 2 < Lh) get_row(r + 2, TP2);                                          \
+    if (r < Lh) {                                                                 \
+      if (r == 0 || r == Lh - 1) copy_row<T, K>(TC, BR);                          \
+      else row_update<T, K, DYN>(TM1, TC, TP1, BR, wt, lc);                       \
+    }                                                                             \
+    if (r >= 2 && r - 2 < Lh) {                                                   \
+      if (r - 2 == 0 || r - 2 == Lh - 1) put_row(r - 2, BM2);                     \
+      else {                                                                      \
+        row_update<T, K, DYN>(BM3, BM2, BM1, o, wt, lc);                          \
+        put_row(r - 2, o);                                                        \
+      }                                                                           \
+    }                                                                             \
+    ++r;                                                                          \
+  }
+#define DTB_PIPE_STEADY(TM1, TC, TP1, TP2, BR, BM1, BM2, BM3)                     \
+  {                                                                               \
+    get_row_nosync(r + 2, TP2);                                                   \
+    row_update2<T, K, DYN>(TM1, TC, TP1, BR, BM3, BM2, BM1, o, wt, lc);           \
+    put_row_nosync(r - 2, o);                                                     \
+    ++r;                                                                          \
+  }
+    // slots at iteration r (mod 4): r%4==0: (t3,t0,t1,t2, b0,b3,b2,b1)
+    //   r%4==1: (t0,t1,t2,t3, b1,b0,b3,b2)  r%4==2: (t1,t2,t3,t0, b2,b1,b0,b3)
+    //   r%4==3: (t2,t3,t0,t1, b3,b2,b1,b0)
+    int r = 0;
+    // prologue r = 0..3 (frozen row 0, first L2 rows)
+    DTB_PIPE_ITER(t3, t0, t1, t2, b0, b3, b2, b1)
+    DTB_PIPE_ITER(t0, t1, t2, t3, b1, b0, b3, b2)
+    DTB_PIPE_ITER(t1, t2, t3, t0, b2, b1, b0, b3)
+    DTB_PIPE_ITER(t2, t3, t0, t1, b3, b2, b1, b0)
+    // steady: r .. r+3 all interior (r-2 >= 1, r+3+2 < Lh, r+3 < Lh-1)
+    while (r + 6 < Lh) {
+      // one flow-control handshake per 4 rows: inputs r+2..r+5, outputs r-2..r+1
+      wait_in(r + 5);
+      wait_out(r + 1);
+      DTB_PIPE_STEADY(t3, t0, t1, t2, b0, b3, b2, b1)
+      DTB_PIPE_STEADY(t0, t1, t2, t3, b1, b0, b3, b2)
+      DTB_PIPE_STEADY(t1, t2, t3, t0, b2, b1, b0, b3)
+      DTB_PIPE_STEADY(t2, t3, t0, t1, b3, b2, b1, b0)
+      release_in(r);       // rows < r are consumed (r+0, r+1 may still be loading)
+      release_out(r - 2);  // outputs < r-2 written
+    }
+    // tail until every output row is out (r = Lh + 1 is the last iteration)
+    while (r <= Lh + 1) {
+      DTB_PIPE_ITER(t3, t0, t1, t2, b0, b3, b2, b1)
+      if (r > Lh + 1) break;
+      DTB_PIPE_ITER(t0, t1, t2, t3, b1, b0, b3, b2)
+      if (r > Lh + 1) break;
+      DTB_PIPE_ITER(t1, t2, t3, t0, b2, b1, b0, b3)
+      if (r > Lh + 1) break;
+      DTB_PIPE_ITER(t2, t3, t0, t1, b3, b2, b1, b0)
+    }
+#undef DTB_PIPE_ITER
+#undef DTB_PIPE_STEADY
+  }
+  if (first) pipe_wait_group<0>();  // drain empty tail groups
+  if (!first && lane == 0) st_release_cta(cons + stage, seq0 + Lh);  // whole tile consumed
+}
+
+}  // namespace dtb

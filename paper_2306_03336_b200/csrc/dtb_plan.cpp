@@ -75,6 +75,9 @@ namespace {
 
 struct Shape { int K; int warps; };
 
+constexpr int kPipeRing0Rows = 16;  // dtb_pipe.cuh kRing0Rows
+constexpr int kPipeRingRows = 8;    // dtb_pipe.cuh kRingRows
+
 // kernel shapes compiled into libdtb_b200.so (dtb_kernels.cu dispatch)
 std::vector<Shape> shapes_for(int elem) {
   std::vector<Shape> v;
@@ -246,8 +249,13 @@ bool plan_streaming(int64_t nx, int64_t ny, int elem, int64_t steps, const DevIn
           const double store_b = (double)(sx.max_load - 2 * h) * (sy.max_load - 2 * h) * elem;
           // per-tile memory time at this SM's share of HBM bandwidth
           const double mem_cta = (load_b + store_b) / (kHbmBytesPerClk / slots);
-          // double-buffered: the next tile's load overlaps this tile's compute
-          const double per_tile = occ == 2 ? std::max(tc, mem_cta) + 500.0 : tc + mem_cta;
+          // double-buffered: the next tile's load overlaps this tile's compute.
+          // Calibrated on B200 (tools/sweep_bench.py DTB_TRACE=1, round 1): each
+          // tile also pays ~10k cycles of copy issue, pipeline fill and band
+          // prologue/epilogue, and the per-CTA copies reach ~half the share
+          // of HBM bandwidth the model assumes.
+          const double per_tile = (occ == 2 ? std::max(tc, 2.0 * mem_cta) : tc + 2.0 * mem_cta)
+                                  + 10000.0;
           const double pass = waves * per_tile + mem_cta + 6000.0;
           const double per_step = pass / hh;
           const double cpc = (double)nx * ny / per_step;
@@ -274,6 +282,50 @@ bool plan_streaming(int64_t nx, int64_t ny, int elem, int64_t steps, const DevIn
   return found;
 }
 
+// Pipelined streaming (dtb_pipe.cuh): S = 4 stage warps per pipeline, two
+// pipelines per CTA, h = 8 steps per pass; tiles are column strips cut into
+// a few long segments so that there are about two pipelines' worth of
+// segments per SM.
+bool plan_pipe(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& dev, Plan& best) {
+  const int K = elem == 8 ? 4 : 8, W = 16, S = 4, P = W / S, h = 2 * S;
+  const int Lw_max = 32 * K;
+  const int per = Lw_max - 2 * h;
+  Split sx;
+  int ntx = (int)std::max<int64_t>(1, (nx + per - 1) / per - 1);
+  for (; ntx <= nx; ++ntx)
+    if (make_split((int)nx, ntx, h, K, Lw_max, 1, sx, 0, 16 / elem)) break;
+  if (ntx > nx) return false;
+  const int64_t want = (int64_t)dev.sms * P;
+  int nseg = (int)std::max<int64_t>(1, want / ntx);  // at most one tile per pipeline
+  nseg = (int)std::min<int64_t>(nseg, std::max<int64_t>(1, ny / (2 * h)));
+  Split sy;
+  for (; nseg >= 1; --nseg)
+    if (make_split((int)ny, nseg, h, 1, 1 << 30, nseg > 1 ? h : 1, sy)) break;
+  if (nseg < 1) return false;
+  best.mode = 3;
+  best.elem = elem;
+  best.K = K;
+  best.warps = W;
+  best.h = h;
+  best.sx = sx;
+  best.sy = sy;
+  const int64_t ntiles = (int64_t)ntx * nseg;
+  best.ctas = (int)std::min<int64_t>(dev.sms, (ntiles + P - 1) / P);
+  best.ctas_per_sm = 1;
+  best.smem_bytes = (int64_t)(12 + (S - 1) * 12) * Lw_max * elem * P;
+  // cost: all lane-cells of every pass at ~70% of the FP issue rate + fill
+  double lane_cells = 0;
+  for (int i = 0; i < sx.n; ++i)
+    for (int j = 0; j < sy.n; ++j)
+      lane_cells += 32.0 * K * (sy.l1[j] - sy.l0[j]);
+  // issue-efficiency calibrated on B200 (round 1: 16 warps, 4 pipelines/CTA)
+  const double rate = (elem == 8 ? 64.0 * 0.49 : 128.0 * 0.37) / 9.0 * dev.sms;
+  best.cycles_per_step = lane_cells / rate + 2000.0 / h;
+  best.cells_per_clk = (double)nx * ny / best.cycles_per_step;
+  (void)steps;
+  return true;
+}
+
 }  // namespace
 
 bool make_plan(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& dev, int force,
@@ -294,8 +346,20 @@ bool make_plan(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& d
     p.elem = elem;
     p.h = 1;
     ok = true;
+  } else if (force == 3) {
+    ok = plan_pipe(nx, ny, elem, steps, dev, p);
+  } else if (force == 4) {
+    ok = plan_resident(nx, ny, elem, steps, dev, depth, p);
+  } else if (force == 1) {
+    ok = plan_streaming(nx, ny, elem, steps, dev, depth, p);
   } else {
-    if (force == 0) ok = plan_resident(nx, ny, elem, steps, dev, depth, p);
+    // auto: smem-resident when the grid fits aggregate smem; otherwise the
+    // pipelined streaming kernel (measured faster than the tile-sweep
+    // streaming kernel on B200: 0.85 vs 0.64 Tcells/s fp64 at 16384^2), with
+    // the tile sweep as the fallback (a forced depth other than 8, tiny grids)
+    ok = plan_resident(nx, ny, elem, steps, dev, depth, p);
+    if (!ok && (depth == 0 || depth == 8) && nx >= 64 && ny >= 64)
+      ok = plan_pipe(nx, ny, elem, steps, dev, p);
     if (!ok) ok = plan_streaming(nx, ny, elem, steps, dev, depth, p);
   }
   if (!ok) {

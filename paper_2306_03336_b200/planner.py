@@ -181,7 +181,7 @@ def tile_active_region(tile, step: int, valid) -> Rect:
 
 # --- the plan that actually runs on the B200 ---------------------------------
 
-MODES = {0: "resident", 1: "streaming", 2: "naive"}
+MODES = {0: "resident", 1: "streaming", 2: "naive", 3: "pipe"}
 
 
 @dataclass(frozen=True)

@@ -213,3 +213,24 @@ def test_device_tensor_entry_and_gpu_fill():
     j2d5pt_device(a, b, nx, ny, MIXED, 33)
     torch.cuda.synchronize()
     assert same(b.cpu().numpy(), jacobi_c(host.data, MIXED.astuple(), 33))
+
+
+PIPE = _native.FLAG_FORCE_PIPE
+
+
+@pytest.mark.parametrize("nx,ny", [(1, 1), (3, 7), (9, 7), (64, 48), (129, 64), (300, 257),
+                                   (1000, 37), (600, 2000)])
+def test_pipe_kernel_matches_oracle(nx, ny):
+    g = rgrid(nx, ny, nx * 7 + ny, ghost=0.375)
+    for steps in (1, 2, 3, 7, 8, 9, 17):
+        want = jacobi_c(g.data, MIXED.astuple(), steps)
+        out, _ = run_dtb_b200(g, MIXED, steps, flags=PIPE)
+        assert same(out.data, want), (nx, ny, steps)
+
+
+def test_pipe_kernel_fp32_and_large():
+    g = rgrid(4000, 3000, 5)
+    out, _ = run_dtb_b200(g, W02, 24, flags=PIPE)
+    assert same(out.data, jacobi_c(g.data, W02.astuple(), 24))
+    out, _ = run_dtb_b200(g, W02, 16, flags=PIPE, dtype=np.float32)
+    assert same(out.data.astype(np.float32), jacobi_c(g.data, W02.astuple(), 16, np.float32))

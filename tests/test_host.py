@@ -55,7 +55,7 @@ def test_native_planner_resident_for_c3a_fp32():
 def test_native_planner_streams_large_domains():
     for nx, elem in ((16384, 8), (8192, 4), (32768, 8)):
         p = plan_b200(nx, nx, elem, 1000, 1)
-        assert p.mode == "streaming", (nx, elem)
+        assert p.mode in ("pipe", "streaming"), (nx, elem)
         assert p.halo >= 2
 
 
