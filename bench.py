@@ -62,6 +62,22 @@ def measured_peaks():
     return peaks
 
 
+def ncu_traffic(kernel, dtype):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed ncu --set full capture (profiles/r01/ncu_summary.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "ncu_summary.json")) as fh:
+            summ = json.load(fh)
+    except (OSError, ValueError):
+        return None, None
+    tag = "double" if dtype == "f64" else "float"
+    for name, rec in summ.items():
+        if name.startswith(kernel + "<" + tag):
+            return rec["dram_bytes_read"] + rec["dram_bytes_write"], \
+                f"{rec['capture']} ({rec['workload']}; per launch, GB-scale inputs stay L2-resident for C2)"
+    return None, None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -377,17 +393,20 @@ def run_b200(args):
         "fp_pipe": {"achieved": cells_per_s * 9 / 1e9, "peak": fp_peak, "unit": "Gop/s",
                     "ops_per_cell": 9, "peak_src": "microbench DMUL/DADD (profiles/r01_microbench_peaks.log)"},
         "hbm": {"achieved": cells_per_s * 2 * elem / max(plan.halo, 1) / 1e9
-                if plan.mode == "streaming" else grid_bytes * 2 / kernel_s / 1e9,
+                if plan.mode in ("streaming", "pipe") else grid_bytes * 2 / kernel_s / 1e9,
                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "peak_src": peaks["hbm_src"]},
     }
     for r in rooflines.values():
         r["frac"] = r["achieved"] / r["peak"]
     if plan.mode == "resident":
+        # the north star's denominator: shared-memory bandwidth at 16 B/cell
         main = dict(rooflines["smem"], bound="smem")
     else:
-        main = dict(rooflines["hbm"], bound="hbm")
-    main["traffic"] = None
-    main["kernel"] = "resident_kernel" if plan.mode == "resident" else "stream_kernel"
+        # streaming passes are FP-issue bound (HBM at 2*elem/h B/cell is far below peak)
+        main = dict(rooflines["fp_pipe"], bound="fp64_pipe" if elem == 8 else "fp32_pipe")
+    main["kernel"] = {"resident": "resident_kernel", "pipe": "pipe_kernel"}.get(plan.mode,
+                                                                                "stream_kernel")
+    main["traffic"], main["traffic_src"] = ncu_traffic(main["kernel"], dtype)
     line = {
         "metric": METRIC, "value": value, "unit": "GCells/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,

@@ -43,8 +43,9 @@
 #define DTB_FASTPATH 1  // static sweep schedule for bands of 4k rows
 #endif
 #ifndef DTB_PUBREG
-#define DTB_PUBREG 0    // resident publish: 0 smem pass after the epoch, 1 from registers
-                        // inside the last sweep, 2 each warp right after its own last sweep
+#define DTB_PUBREG 3    // resident publish: 0 smem pass after the epoch, 1 from registers
+                        // inside the last sweep, 2 each warp right after its own last sweep,
+                        // 3 as 2 with a per-warp release-add on the epoch flag (no CTA barrier)
 #endif
 #ifndef DTB_RING
 #define DTB_RING 2      // resident halo refresh: 0 generic, 1 ring copy after one wait,
@@ -284,7 +285,8 @@ struct Publisher {
   int64_t pitch;
   int own0, own1, top1, bot0;
   uint32_t full_mask, side_mask;
-  // mode 2: publish the band's own rows [ya, yb) from smem (they are final once
+  int* flag;        // mode 3: this CTA's epoch flag (per-warp release-add)
+  // mode 2/3: publish the band's own rows [ya, yb) from smem (they are final once
   // the band's last sweep is done: no other warp writes them)
   __device__ __forceinline__ void put_band(const LaneAddr<T, K>& la, int ya, int yb) const {
     const int r0 = max(ya, own0), r1 = min(yb, own1);
@@ -551,9 +553,17 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
     for (; s + 2 <= steps; s += 2) {
       if (band_pub && s + 2 == steps) sweep2<T, K, DYN, true>(la, Lh, ya, yb, act, wt, lc, pb);
       else sweep2<T, K, DYN, false>(la, Lh, ya, yb, act, wt, lc, pb);
-      if (DTB_PUBREG == 2 && pub && act && s + 2 == steps) {
-        pub->put_band(la, ya, yb);  // this warp's rows are final: publish them now
-        __threadfence();
+      if (DTB_PUBREG >= 2 && pub && s + 2 == steps) {
+        if (act) pub->put_band(la, ya, yb);  // this warp's rows are final: publish now
+        if (DTB_PUBREG == 2) {
+          __threadfence();
+        } else {
+          // each warp releases its own stores and bumps the CTA's epoch flag;
+          // neighbours wait for nwarps bumps per epoch (no CTA barrier first)
+          __syncwarp();
+          if (lc.lane == 0)
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
+        }
       }
       __syncthreads();
     }
@@ -566,9 +576,15 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
     for (; s < steps; ++s) {
       if (band_pub && s + 1 == steps) sweep1<T, K, DYN, true>(la, Lh, ya, yb, warp < nb1, wt, lc, pb);
       else sweep1<T, K, DYN, false>(la, Lh, ya, yb, warp < nb1, wt, lc, pb);
-      if (DTB_PUBREG == 2 && pub && warp < nb1 && s + 1 == steps) {
-        pub->put_band(la, ya, yb);
-        __threadfence();
+      if (DTB_PUBREG >= 2 && pub && s + 1 == steps) {
+        if (warp < nb1) pub->put_band(la, ya, yb);
+        if (DTB_PUBREG == 2) {
+          __threadfence();
+        } else {
+          __syncwarp();
+          if (lc.lane == 0)
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
+        }
       }
       __syncthreads();
     }

@@ -605,6 +605,10 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
   pub.bot0 = oy1 - bb;
   pub.full_mask = 0;
   pub.side_mask = 0;
+  pub.flag = flags + blockIdx.x;
+  // flag value that marks "epoch e published": e (CTA-level release) or
+  // e * warps (mode 3: one release-add per warp)
+  const int flag_per_epoch = (DTB_PUBREG == 3 && !poison) ? (int)(blockDim.x >> 5) : 1;
   {
     const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -653,7 +657,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     if (DTB_FENCE == 1) __threadfence();
     __syncthreads();
     DTB_MARK(t_pbar)
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && flag_per_epoch == 1) {
       if (DTB_FENCE == 9) *(volatile int*)(flags + blockIdx.x) = epoch;
       else st_release(flags + blockIdx.x, epoch);
     }
@@ -662,8 +666,9 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
       // 2+3. per-direction: warp k waits for the neighbour owning halo region k
       // and immediately streams that region in (overlaps the 8 waits and loads)
       DTB_MARK(t_wait)
-      refresh_by_direction<T, K>(tile, xb, pitch, gx0, gy0, flags, epoch, geo.ntx, geo.nty, tx,
-                                 ty, ry0, oy0, oy1, ry1, rx0, ox0, ox1, rx1);
+      refresh_by_direction<T, K>(tile, xb, pitch, gx0, gy0, flags, epoch * flag_per_epoch,
+                                 geo.ntx, geo.nty, tx, ty, ry0, oy0, oy1, ry1, rx0, ox0, ox1,
+                                 rx1);
       __syncthreads();
     } else {
     // 2. wait for the (up to 8) neighbours of this epoch
@@ -672,7 +677,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
       const int nxt = tx + dx, nyt = ty + dy;
       if (nxt >= 0 && nxt < geo.ntx && nyt >= 0 && nyt < geo.nty) {
         const int* f = flags + nyt * geo.ntx + nxt;
-        while (ld_acquire(f) < epoch) __nanosleep(32);
+        while (ld_acquire(f) < epoch * flag_per_epoch) __nanosleep(32);
       }
     }
     __syncthreads();
