@@ -290,23 +290,43 @@ struct Publisher {
   // the band's last sweep is done: no other warp writes them)
   __device__ __forceinline__ void put_band(const LaneAddr<T, K>& la, int ya, int yb) const {
     const int r0 = max(ya, own0), r1 = min(yb, own1);
-    for (int row = r0; row < r1; ++row) {
-      const uint32_t m = (row < top1 || row >= bot0) ? full_mask : side_mask;
-      if (__any_sync(0xffffffffu, m != 0u)) {
-        T v[K];
-        load_row<T, K>(la, row, v);
-        T* p = g + (int64_t)row * pitch;
+    // lanes with nothing to publish in any of these rows skip the loop
+    if ((full_mask | side_mask) == 0u) return;
+    int row = r0;
+    for (; row + 4 <= r1; row += 4) {  // 4 rows of LDS in flight, then the stores
+      T v[4][K];
 #pragma unroll
-        for (int e = 0; e < K; ++e) st_pred(((m >> e) & 1u) != 0, p + e, v[e]);
+      for (int u = 0; u < 4; ++u) load_row<T, K>(la, row + u, v[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rr = row + u;
+        const uint32_t m = (rr < top1 || rr >= bot0) ? full_mask : side_mask;
+        T* p = g + (int64_t)rr * pitch;
+#pragma unroll
+        for (int e = 0; e < K; ++e) st_pred(((m >> e) & 1u) != 0, p + e, v[u][e]);
       }
+    }
+    for (; row < r1; ++row) {
+      T v[K];
+      load_row<T, K>(la, row, v);
+      const uint32_t m = (row < top1 || row >= bot0) ? full_mask : side_mask;
+      T* p = g + (int64_t)row * pitch;
+#pragma unroll
+      for (int e = 0; e < K; ++e) st_pred(((m >> e) & 1u) != 0, p + e, v[e]);
     }
   }
   __device__ __forceinline__ bool covers(int ya, int yb) const {
     return (ya < top1 && yb > own0) || (ya < own1 && yb > bot0);
   }
   __device__ __forceinline__ void put(int row, const T (&v)[K]) const {
-    const bool in = (row >= own0 && row < top1) || (row >= bot0 && row < own1);
-    const uint32_t m = in ? full_mask : 0u;
+    uint32_t m;
+    if (DTB_PUBREG == 4) {  // every owned row: full rows in the top/bottom band, else sides
+      const bool own = row >= own0 && row < own1;
+      m = own ? ((row < top1 || row >= bot0) ? full_mask : side_mask) : 0u;
+    } else {
+      const bool in = (row >= own0 && row < top1) || (row >= bot0 && row < own1);
+      m = in ? full_mask : 0u;
+    }
     T* p = g + (int64_t)row * pitch;
 #pragma unroll
     for (int e = 0; e < K; ++e) st_pred(((m >> e) & 1u) != 0, p + e, v[e]);
@@ -549,13 +569,15 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
     int ya, yb;
     band_rows4(Lh, nb2, min(warp, nb2 - 1), ya, yb);
     const bool act = warp < nb2;
-    const bool band_pub = DTB_PUBREG == 1 && pub && pub->covers(ya, yb);
+    const bool band_pub = pub && ((DTB_PUBREG == 1 && pub->covers(ya, yb)) || DTB_PUBREG == 4);
     for (; s + 2 <= steps; s += 2) {
       if (band_pub && s + 2 == steps) sweep2<T, K, DYN, true>(la, Lh, ya, yb, act, wt, lc, pb);
       else sweep2<T, K, DYN, false>(la, Lh, ya, yb, act, wt, lc, pb);
       if (DTB_PUBREG >= 2 && pub && s + 2 == steps) {
-        if (act) pub->put_band(la, ya, yb);  // this warp's rows are final: publish now
-        if (DTB_PUBREG == 2) {
+        if (act && DTB_PUBREG != 4) pub->put_band(la, ya, yb);  // rows final: publish now
+        if (DTB_PUBREG == 5) {
+          // stores only; one CTA-level release after the closing barrier
+        } else if (DTB_PUBREG == 2) {
           __threadfence();
         } else {
           // each warp releases its own stores and bumps the CTA's epoch flag;
@@ -572,13 +594,14 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
     const int nb1 = max(1, min(nw, rows));
     int ya, yb;
     band_rows(Lh, nb1, min(warp, nb1 - 1), ya, yb);
-    const bool band_pub = DTB_PUBREG == 1 && pub && pub->covers(ya, yb);
+    const bool band_pub = pub && ((DTB_PUBREG == 1 && pub->covers(ya, yb)) || DTB_PUBREG == 4);
     for (; s < steps; ++s) {
       if (band_pub && s + 1 == steps) sweep1<T, K, DYN, true>(la, Lh, ya, yb, warp < nb1, wt, lc, pb);
       else sweep1<T, K, DYN, false>(la, Lh, ya, yb, warp < nb1, wt, lc, pb);
       if (DTB_PUBREG >= 2 && pub && s + 1 == steps) {
-        if (warp < nb1) pub->put_band(la, ya, yb);
-        if (DTB_PUBREG == 2) {
+        if (warp < nb1 && DTB_PUBREG != 4) pub->put_band(la, ya, yb);
+        if (DTB_PUBREG == 5) {
+        } else if (DTB_PUBREG == 2) {
           __threadfence();
         } else {
           __syncwarp();

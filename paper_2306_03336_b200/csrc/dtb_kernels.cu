@@ -608,7 +608,8 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
   pub.flag = flags + blockIdx.x;
   // flag value that marks "epoch e published": e (CTA-level release) or
   // e * warps (mode 3: one release-add per warp)
-  const int flag_per_epoch = (DTB_PUBREG == 3 && !poison) ? (int)(blockDim.x >> 5) : 1;
+  const int flag_per_epoch =
+      ((DTB_PUBREG == 3 || DTB_PUBREG == 4) && !poison) ? (int)(blockDim.x >> 5) : 1;
   {
     const int lane = threadIdx.x & 31;
 #pragma unroll
