@@ -43,9 +43,12 @@
 #define DTB_FASTPATH 1  // static sweep schedule for bands of 4k rows
 #endif
 #ifndef DTB_PUBREG
-#define DTB_PUBREG 3    // resident publish: 0 smem pass after the epoch, 1 from registers
+#define DTB_PUBREG 6    // resident publish: 0 smem pass after the epoch, 1 from registers
                         // inside the last sweep, 2 each warp right after its own last sweep,
-                        // 3 as 2 with a per-warp release-add on the epoch flag (no CTA barrier)
+                        // 3 as 2 with a per-warp release-add on the epoch flag (no CTA barrier),
+                        // 4 every owned row from registers + release-add, 5 as 2 with one
+                        // CTA-level release, 6 as 3 with the side columns flattened across
+                        // lanes (fewest stores; the default)
 #endif
 #ifndef DTB_RING
 #define DTB_RING 2      // resident halo refresh: 0 generic, 1 ring copy after one wait,
@@ -258,6 +261,48 @@ __device__ __forceinline__ void copy_row(const T (&a)[K], T (&b)[K]) {
   for (int e = 0; e < K; ++e) b[e] = a[e];
 }
 
+#ifndef DTB_XCHG
+#define DTB_XCHG 0  // resident exchange: 0 mirror grid + release/acquire epoch flags,
+                    // 1 stamped words (every 8-byte word carries the epoch stamp in its
+                    // high half: no fence, no flag; readers check each word)
+#endif
+
+// Stamped exchange words: value bits in the low 32 bits, the epoch stamp in the
+// high 32; fp64 values take two words (lo, hi). Each 8-byte word is one
+// single-copy-atomic access, so a reader that sees the stamp sees the payload.
+template <typename T>
+struct Stamped {
+  static constexpr int WPV = sizeof(T) == 8 ? 2 : 1;  // words per value
+};
+__device__ __forceinline__ void st_stamped(uint64_t* p, double v, uint32_t stamp) {
+  const uint64_t b = (uint64_t)__double_as_longlong(v), hi = (uint64_t)stamp << 32;
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p),
+               "l"(hi | (b & 0xffffffffull)), "l"(hi | (b >> 32)) : "memory");
+}
+__device__ __forceinline__ void st_stamped(uint64_t* p, float v, uint32_t stamp) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p),
+               "l"(((uint64_t)stamp << 32) | __float_as_uint(v)) : "memory");
+}
+struct StampedLoad {  // one value's words in flight
+  uint64_t a, b;
+};
+__device__ __forceinline__ void ld_stamped(const uint64_t* p, StampedLoad& w, double) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w.a), "=l"(w.b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void ld_stamped(const uint64_t* p, StampedLoad& w, float) {
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w.a) : "l"(p) : "memory");
+  w.b = w.a;
+}
+__device__ __forceinline__ bool stamped_ok(const StampedLoad& w, uint32_t stamp) {
+  return (uint32_t)(w.a >> 32) == stamp && (uint32_t)(w.b >> 32) == stamp;
+}
+__device__ __forceinline__ double stamped_value(const StampedLoad& w, double) {
+  return __longlong_as_double((long long)((w.a & 0xffffffffull) | (w.b << 32)));
+}
+__device__ __forceinline__ float stamped_value(const StampedLoad& w, float) {
+  return __uint_as_float((uint32_t)w.a);
+}
+
 // Publisher: during the last sweep of a resident epoch, every freshly
 // computed row that lies in the CTA's owned band (the cells its neighbours'
 // halos cover) is also stored straight from registers to the L2 exchange
@@ -288,10 +333,49 @@ struct Publisher {
   int* flag;        // mode 3: this CTA's epoch flag (per-warp release-add)
   // mode 2/3: publish the band's own rows [ya, yb) from smem (they are final once
   // the band's last sweep is done: no other warp writes them)
+  // mode 6: side columns flattened across lanes (lane i -> element i of the
+  // band's (row, side column) list), so one warp store covers 32 / (wl + wr)
+  // rows instead of one
+  T* g0;            // exchange buffer at (tile row 0, tile column 0)
+  uint64_t* x;      // DTB_XCHG 1: stamped-word buffer at (tile row 0, tile column 0)
+  uint32_t stamp;   // DTB_XCHG 1: this epoch's stamp
+  int cl0, wl, cr0, wr;  // side columns [cl0, cl0 + wl) and [cr0, cr0 + wr)
+  __device__ __forceinline__ void put_sides(const LaneAddr<T, K>& la, int r0, int r1) const {
+    typedef Tile<T, K> L;
+    const int w = wl + wr, n = (r1 - r0) * w;
+    const int lane = threadIdx.x & 31;
+#pragma unroll 2
+    for (int i = lane; i < n; i += 32) {
+      const int q = i / w, j = i - q * w, r = r0 + q;
+      const int c = j < wl ? cl0 + j : cr0 + (j - wl);
+      T v;
+      if (sizeof(T) == 8) {
+        double d;
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(d) : "r"(la.base + (uint32_t)(L::at(r, c) * 8)));
+        v = (T)d;
+      } else {
+        float f;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(f) : "r"(la.base + (uint32_t)(L::at(r, c) * 4)));
+        v = (T)f;
+      }
+      if (DTB_XCHG == 1) st_stamped(x + ((int64_t)r * pitch + c) * Stamped<T>::WPV, v, stamp);
+      else st_pred(true, g0 + (int64_t)r * pitch + c, v);
+    }
+  }
   __device__ __forceinline__ void put_band(const LaneAddr<T, K>& la, int ya, int yb) const {
-    const int r0 = max(ya, own0), r1 = min(yb, own1);
+    if (DTB_PUBREG == 6) {
+      const int r0 = max(ya, own0), r1 = min(yb, own1);
+      const int s0 = max(r0, top1), s1 = min(r1, bot0);
+      if (s0 < s1) put_sides(la, s0, s1);
+      put_rows(la, r0, min(r1, top1));
+      put_rows(la, max(r0, bot0), r1);
+      return;
+    }
+    put_rows(la, max(ya, own0), min(yb, own1));
+  }
+  __device__ __forceinline__ void put_rows(const LaneAddr<T, K>& la, int r0, int r1) const {
     // lanes with nothing to publish in any of these rows skip the loop
-    if ((full_mask | side_mask) == 0u) return;
+    if ((full_mask | side_mask) == 0u || r0 >= r1) return;
     int row = r0;
     for (; row + 4 <= r1; row += 4) {  // 4 rows of LDS in flight, then the stores
       T v[4][K];
@@ -301,6 +385,13 @@ struct Publisher {
       for (int u = 0; u < 4; ++u) {
         const int rr = row + u;
         const uint32_t m = (rr < top1 || rr >= bot0) ? full_mask : side_mask;
+        if (DTB_XCHG == 1) {
+          uint64_t* q = x + ((int64_t)rr * pitch + (threadIdx.x & 31) * K) * Stamped<T>::WPV;
+#pragma unroll
+          for (int e = 0; e < K; ++e)
+            if ((m >> e) & 1u) st_stamped(q + e * Stamped<T>::WPV, v[u][e], stamp);
+          continue;
+        }
         T* p = g + (int64_t)rr * pitch;
 #pragma unroll
         for (int e = 0; e < K; ++e) st_pred(((m >> e) & 1u) != 0, p + e, v[u][e]);
@@ -310,6 +401,13 @@ struct Publisher {
       T v[K];
       load_row<T, K>(la, row, v);
       const uint32_t m = (row < top1 || row >= bot0) ? full_mask : side_mask;
+      if (DTB_XCHG == 1) {
+        uint64_t* q = x + ((int64_t)row * pitch + (threadIdx.x & 31) * K) * Stamped<T>::WPV;
+#pragma unroll
+        for (int e = 0; e < K; ++e)
+          if ((m >> e) & 1u) st_stamped(q + e * Stamped<T>::WPV, v[e], stamp);
+        continue;
+      }
       T* p = g + (int64_t)row * pitch;
 #pragma unroll
       for (int e = 0; e < K; ++e) st_pred(((m >> e) & 1u) != 0, p + e, v[e]);
@@ -579,6 +677,8 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
           // stores only; one CTA-level release after the closing barrier
         } else if (DTB_PUBREG == 2) {
           __threadfence();
+        } else if (DTB_XCHG == 1) {
+          // stamped words need no fence or flag
         } else {
           // each warp releases its own stores and bumps the CTA's epoch flag;
           // neighbours wait for nwarps bumps per epoch (no CTA barrier first)
@@ -603,6 +703,7 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
         if (DTB_PUBREG == 5) {
         } else if (DTB_PUBREG == 2) {
           __threadfence();
+        } else if (DTB_XCHG == 1) {
         } else {
           __syncwarp();
           if (lc.lane == 0)

@@ -163,6 +163,12 @@ __device__ __forceinline__ double lds_elem(uint32_t a, double) {
   asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
   return v;
 }
+__device__ __forceinline__ void sts_elem(uint32_t a, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void sts_elem(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
 __device__ __forceinline__ float lds_elem(uint32_t a, float) {
   float v;
   asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
@@ -236,6 +242,11 @@ __device__ __forceinline__ void s2g_rows(const T* tile, T* __restrict__ g, int64
 // SW, SE) of the ring is owned by one neighbour; warp k polls that
 // neighbour's epoch flag and streams the region in with cp.async as soon as
 // it is published, so the eight waits and loads overlap.
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -279,7 +290,8 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
                                                      int64_t pitch, int gx0, int gy0,
                                                      const int* flags, int epoch, int ntx, int nty,
                                                      int tx, int ty, int ry0, int oy0, int oy1,
-                                                     int ry1, int rx0, int ox0, int ox1, int rx1) {
+                                                     int ry1, int rx0, int ox0, int ox1, int rx1,
+                                                     unsigned long long* mark = nullptr) {
   typedef Tile<T, K> L;
 #ifndef DTB_SIDE_PARTS
 #define DTB_SIDE_PARTS 1
@@ -315,14 +327,166 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
     if (r1 <= r0 || c1 <= c0 || nxt < 0 || nxt >= ntx || nyt < 0 || nyt >= nty) continue;
     const int nb = nyt * ntx + nxt;
     if (nb != polled) {
-      if (lane == 0)
-        while (ld_acquire_gpu(flags + nb) < epoch) __nanosleep(32);
+#ifndef DTB_POLL
+#define DTB_POLL 0  // 0: acquire load per poll; 1: relaxed polls + one acquire load;
+                    // 2: relaxed polls (no sleep) + one acquire load
+#endif
+      if (lane == 0) {
+        if (DTB_POLL == 0) {
+          while (ld_acquire_gpu(flags + nb) < epoch) __nanosleep(32);
+        } else {
+          while (ld_relaxed_gpu(flags + nb) < epoch)
+            if (DTB_POLL == 1) __nanosleep(32);
+          (void)ld_acquire_gpu(flags + nb);
+        }
+      }
       __syncwarp();
+      if (mark && polled < 0) *mark = clock64();
       polled = nb;
     }
     warp_g2s_chunks<T, K>(sbase, g, pitch, gx0, gy0, r0, r1, c0, c1, vec, lane);
   }
   cp_async_wait_all();
+}
+
+// Stamped-word refresh of the halo rectangle [r0, r1) x [c0, c1) (tile
+// coordinates) by one warp: kBatch words in flight per lane, each value
+// re-polled until its words carry this epoch's stamp, then stored to smem.
+template <typename T, int K>
+__device__ __forceinline__ void warp_refresh_stamped(uint32_t sbase, const uint64_t* __restrict__ x,
+                                                     int64_t pitch, int gx0, int gy0, int r0,
+                                                     int r1, int c0, int c1, uint32_t stamp,
+                                                     int lane) {
+  typedef Tile<T, K> L;
+  constexpr int kBatch = 8, WPV = Stamped<T>::WPV;
+  const int w = c1 - c0, n = (r1 - r0) * w;
+  for (int base = lane; base < n; base += 32 * kBatch) {
+    StampedLoad v[kBatch];
+    const uint64_t* src[kBatch];
+    uint32_t dst[kBatch];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int i = base + 32 * j;
+      const int q = i / w, r = r0 + q, c = c0 + (i - q * w);
+      src[j] = x + ((int64_t)(gy0 + r) * pitch + gx0 + c) * WPV;
+      dst[j] = sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T));
+      if (i < n) ld_stamped(src[j], v[j], T());
+    }
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      if (base + 32 * j < n) {
+        while (!stamped_ok(v[j], stamp)) {
+          __nanosleep(16);
+          ld_stamped(src[j], v[j], T());
+        }
+        sts_elem(dst[j], stamped_value(v[j], T()));
+      }
+    }
+  }
+}
+
+// Halo refresh over stamped words: the (up to 8) ring rectangles are
+// flattened into one index space spread over every thread of the CTA, each
+// thread keeping all its loads in flight at once (one L2 round trip for the
+// whole ring when the neighbours have published); no flags (each word proves
+// its own epoch).
+#ifndef DTB_STAMP_BATCH
+#define DTB_STAMP_BATCH 8
+#endif
+#ifndef DTB_STAMP_SENTINEL
+#define DTB_STAMP_SENTINEL 1
+#endif
+template <typename T, int K>
+__device__ __forceinline__ void refresh_stamped(T* tile, const uint64_t* __restrict__ x,
+                                                int64_t pitch, int gx0, int gy0, uint32_t stamp,
+                                                int ntx, int nty, int tx, int ty, int ry0,
+                                                int oy0, int oy1, int ry1, int rx0, int ox0,
+                                                int ox1, int rx1, unsigned long long* mark) {
+  typedef Tile<T, K> L;
+  constexpr int WPV = Stamped<T>::WPV, kBatch = DTB_STAMP_BATCH;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
+  // rectangles: N, S, NW, NE, SW, SE, W, E (empty when the neighbour is absent)
+  int rr0[8], cc0[8], ww[8], end[8];
+  int total = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    int dx, dy, r0, r1, c0, c1;
+    switch (k) {
+      case 0: dx = 0; dy = -1; r0 = ry0; r1 = oy0; c0 = ox0; c1 = ox1; break;
+      case 1: dx = 0; dy = 1; r0 = oy1; r1 = ry1; c0 = ox0; c1 = ox1; break;
+      case 2: dx = -1; dy = -1; r0 = ry0; r1 = oy0; c0 = rx0; c1 = ox0; break;
+      case 3: dx = 1; dy = -1; r0 = ry0; r1 = oy0; c0 = ox1; c1 = rx1; break;
+      case 4: dx = -1; dy = 1; r0 = oy1; r1 = ry1; c0 = rx0; c1 = ox0; break;
+      case 5: dx = 1; dy = 1; r0 = oy1; r1 = ry1; c0 = ox1; c1 = rx1; break;
+      case 6: dx = -1; dy = 0; r0 = oy0; r1 = oy1; c0 = rx0; c1 = ox0; break;
+      default: dx = 1; dy = 0; r0 = oy0; r1 = oy1; c0 = ox1; c1 = rx1; break;
+    }
+    const int nxt = tx + dx, nyt = ty + dy;
+    const bool on = r1 > r0 && c1 > c0 && nxt >= 0 && nxt < ntx && nyt >= 0 && nyt < nty;
+    rr0[k] = r0;
+    cc0[k] = c0;
+    ww[k] = on ? c1 - c0 : 1;
+    total += on ? (r1 - r0) * (c1 - c0) : 0;
+    end[k] = total;
+#if DTB_STAMP_SENTINEL
+    // thread k first waits on one word of rectangle k (cheap polling); the
+    // bulk loads below then mostly find their stamps on the first try
+    if (on && (int)threadIdx.x == 32 * k) {
+      StampedLoad w;
+      const uint64_t* q = x + ((int64_t)(gy0 + r1 - 1) * pitch + gx0 + c1 - 1) * WPV;
+      ld_stamped(q, w, T());
+      while (!stamped_ok(w, stamp)) {
+        __nanosleep(64);
+        ld_stamped(q, w, T());
+      }
+    }
+#endif
+  }
+#if DTB_STAMP_SENTINEL
+  __syncthreads();
+#endif
+  if (mark) *mark = clock64();
+  for (int base = threadIdx.x; base < total; base += blockDim.x * kBatch) {
+    StampedLoad v[kBatch];
+    const uint64_t* src[kBatch];
+    uint32_t dst[kBatch];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int i = base + (int)blockDim.x * j;
+      int k = 0, st0 = 0;
+#pragma unroll
+      for (int q = 0; q < 7; ++q)
+        if (i >= end[q]) { k = q + 1; st0 = end[q]; }
+      int r0 = rr0[0], c0 = cc0[0], w = ww[0];
+#pragma unroll
+      for (int q = 1; q < 8; ++q)
+        if (k == q) { r0 = rr0[q]; c0 = cc0[q]; w = ww[q]; }
+      const int li = i - st0, qr = li / w, r = r0 + qr, c = c0 + (li - qr * w);
+      src[j] = x + ((int64_t)(gy0 + r) * pitch + gx0 + c) * WPV;
+      dst[j] = sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T));
+      if (i < total) ld_stamped(src[j], v[j], T());
+    }
+    // retire the words that carry the stamp; re-poll the rest together (one
+    // round trip per retry, not one per late word)
+    uint32_t pending = 0;
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j)
+      if (base + (int)blockDim.x * j < total) pending |= 1u << j;
+    while (true) {
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) {
+        if (((pending >> j) & 1u) && stamped_ok(v[j], stamp)) {
+          sts_elem(dst[j], stamped_value(v[j], T()));
+          pending &= ~(1u << j);
+        }
+      }
+      if (!pending) break;
+      __nanosleep(32);
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j)
+        if ((pending >> j) & 1u) ld_stamped(src[j], v[j], T());
+    }
+  }
 }
 
 // Resident publish of the owned band: rows [oy0, t1) and [b0, oy1) in full
@@ -560,7 +724,8 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
 template <typename T, int K, int NW, bool DYN>
 __global__ void __launch_bounds__(NW * 32, 1)
 resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ xb0,
-                T* __restrict__ xb1, int* __restrict__ flags, int64_t pitch, int nx, int ny,
+                T* __restrict__ xb1, uint64_t* __restrict__ xs0, uint64_t* __restrict__ xs1,
+                uint32_t stamp0, int* __restrict__ flags, int64_t pitch, int nx, int ny,
                 Weights<T> wt, int64_t total_steps, int h, int poison,
                 unsigned long long* __restrict__ trace, const __grid_constant__ Geometry geo) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -606,10 +771,15 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
   pub.full_mask = 0;
   pub.side_mask = 0;
   pub.flag = flags + blockIdx.x;
+  pub.cl0 = ox0;
+  pub.wl = bl;
+  pub.cr0 = max(ox1 - br, ox0 + bl);
+  pub.wr = ox1 - pub.cr0;
   // flag value that marks "epoch e published": e (CTA-level release) or
   // e * warps (mode 3: one release-add per warp)
+  const bool stamped = DTB_XCHG == 1 && !poison;
   const int flag_per_epoch =
-      ((DTB_PUBREG == 3 || DTB_PUBREG == 4) && !poison) ? (int)(blockDim.x >> 5) : 1;
+      ((DTB_PUBREG == 3 || DTB_PUBREG == 4 || DTB_PUBREG == 6) && !poison) ? (int)(blockDim.x >> 5) : 1;
   {
     const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -625,7 +795,10 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     const int steps = (int)((total_steps - done) < (int64_t)h ? (total_steps - done) : (int64_t)h);
     const bool last = done + steps >= total_steps;
     T* xb = ((epoch + 1) & 1) ? xb1 : xb0;
-    pub.g = xb + (int64_t)gy0 * pitch + gx0 + (threadIdx.x & 31) * K;
+    pub.x = (((epoch + 1) & 1) ? xs1 : xs0) + ((int64_t)gy0 * pitch + gx0) * Stamped<T>::WPV;
+    pub.stamp = stamp0 + (uint32_t)(epoch + 1);
+    pub.g0 = xb + (int64_t)gy0 * pitch + gx0;
+    pub.g = pub.g0 + (threadIdx.x & 31) * K;
     // 1. compute the epoch; its final sweep publishes the owned band from registers
     advance<T, K, DYN>(tile, Lw, Lh, steps, wt, poison != 0, hl, hr, ht, hb,
                        (last || poison || !DTB_PUBREG) ? nullptr : &pub);
@@ -633,6 +806,19 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     DTB_MARK(t_comp)
     if (last) break;
     ++epoch;
+    if (stamped) {
+      unsigned long long t_s = 0;
+      // 2+3. stamped words: no barrier, fence or flag; each warp polls its
+      // ring tasks' words and stores them as they arrive
+      refresh_stamped<T, K>(tile, (epoch & 1) ? xs1 : xs0, pitch, gx0, gy0,
+                            stamp0 + (uint32_t)epoch, geo.ntx, geo.nty, tx, ty, ry0, oy0, oy1,
+                            ry1, rx0, ox0, ox1, rx1, tracing ? &t_s : nullptr);
+      if (tracing) t_pst += t_s - tc;
+      DTB_MARK(t_wait)
+      __syncthreads();
+      DTB_MARK(t_ref)
+      continue;
+    }
     if (!poison && DTB_PUBREG == 0) {
       const int t1 = min(oy0 + bt, oy1), b0 = max(oy1 - bb, t1);
       publish_band<T, K>(tile, xb, pitch, gx0, gy0, oy0, t1, b0, oy1, ox0, ox0 + bl,
@@ -667,9 +853,16 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
       // 2+3. per-direction: warp k waits for the neighbour owning halo region k
       // and immediately streams that region in (overlaps the 8 waits and loads)
       DTB_MARK(t_wait)
+      unsigned long long t_poll = tc;
       refresh_by_direction<T, K>(tile, xb, pitch, gx0, gy0, flags, epoch * flag_per_epoch,
                                  geo.ntx, geo.nty, tx, ty, ry0, oy0, oy1, ry1, rx0, ox0, ox1,
-                                 rx1);
+                                 rx1, tracing ? &t_poll : nullptr);
+      if (tracing) {
+        const unsigned long long now_ = clock64();
+        t_wait += t_poll - tc;   // warp 0: until its first neighbour flag arrived
+        t_pst += now_ - t_poll;  // warp 0: its loads
+        tc = now_;
+      }
       __syncthreads();
     } else {
     // 2. wait for the (up to 8) neighbours of this epoch
@@ -806,6 +999,38 @@ int arena_get(Arena& a, size_t bytes, void** out) {
   return DTB_OK;
 }
 
+// Stamped-word exchange buffers (DTB_XCHG 1): dedicated per device, zeroed on
+// allocation; every resident epoch ever run on them gets a fresh stamp, so a
+// word left by an earlier epoch or launch can never pass a reader's check.
+struct StampArena {
+  void* p = nullptr;
+  size_t n = 0;
+  uint32_t next = 1;
+};
+StampArena g_stamped[16];
+
+int stamped_get(StampArena& a, size_t bytes, int64_t epochs, cudaStream_t st, uint64_t** out,
+                uint32_t* stamp0) {
+  if (a.n < bytes) {
+    if (a.p) cudaFree(a.p);
+    a.p = nullptr;
+    a.n = 0;
+    CUDA_TRY(cudaMalloc(&a.p, bytes));
+    a.n = bytes;
+    CUDA_TRY(cudaMemsetAsync(a.p, 0, bytes, st));
+    a.next = 1;
+  }
+  if ((int64_t)a.next + epochs + 2 > 0x7fffffffLL) {
+    if (epochs + 3 > 0x7fffffffLL) return fail(DTB_ERANGE, "too many resident epochs (%lld)", (long long)epochs);
+    CUDA_TRY(cudaMemsetAsync(a.p, 0, a.n, st));
+    a.next = 1;
+  }
+  *stamp0 = a.next;
+  a.next += (uint32_t)(epochs + 1);
+  *out = reinterpret_cast<uint64_t*>(a.p);
+  return DTB_OK;
+}
+
 int query_dev(DevInfo& d) {
   int dev = 0, v = 0;
   CUDA_TRY(cudaGetDevice(&dev));
@@ -880,9 +1105,21 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
           reinterpret_cast<char*>(scratch) + ((2 * grid_bytes + flag_bytes + 255) & ~(size_t)255));
       CUDA_TRY(cudaMemsetAsync(trace, 0, trace_bytes, st));
     }
+    // stamped words: (ny + 2) x pitch values x WPV words, two parities
+    const size_t xs_bytes = (size_t)(ny + 2) * pitch * Stamped<T>::WPV * sizeof(uint64_t);
+    uint64_t* xs0 = nullptr;
+    uint32_t stamp0 = 0;
+    if (DTB_XCHG == 1 && !poison) {
+      std::lock_guard<std::mutex> lk(g_mu);
+      int rc = stamped_get(g_stamped[device & 15], 2 * xs_bytes, (steps + p.h - 1) / p.h, st,
+                           &xs0, &stamp0);
+      if (rc) return rc;
+    }
+    uint64_t* xs1 = xs0 ? xs0 + xs_bytes / sizeof(uint64_t) : nullptr;
     int h = p.h;
     int pois = poison ? 1 : 0;
-    void* args[] = {(void*)&d_in, (void*)&d_out, (void*)&xb0, (void*)&xb1, (void*)&flags,
+    void* args[] = {(void*)&d_in, (void*)&d_out, (void*)&xb0, (void*)&xb1, (void*)&xs0,
+                    (void*)&xs1, (void*)&stamp0, (void*)&flags,
                     (void*)&pitch, (void*)&nx, (void*)&ny, (void*)&wt, (void*)&steps,
                     (void*)&h, (void*)&pois, (void*)&trace, (void*)&geo};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(p.ctas), dim3(threads), args,
@@ -1007,6 +1244,12 @@ int dispatch(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_
     return dispatch_dyn<T, KK, WW>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st);
   if constexpr (sizeof(T) == 8) {
     DTB_SHAPE(4, 8)
+#ifdef DTB_W12
+    DTB_SHAPE(4, 12)
+#endif
+#ifdef DTB_W4
+    DTB_SHAPE(4, 4)
+#endif
 #ifdef DTB_WIDE
     DTB_SHAPE(8, 8)
 #endif

@@ -2,6 +2,8 @@
 #include "dtb_plan.h"
 
 #include <algorithm>
+#include <mutex>
+#include <string>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -86,6 +88,12 @@ std::vector<Shape> shapes_for(int elem) {
   // 16 warps (<= 128 registers) and 64 B per lane both spill)
   if (elem == 8) v = {{4, 8}};
   else v = {{8, 8}};
+#ifdef DTB_W12
+  if (elem == 8) v.push_back({4, 12});
+#endif
+#ifdef DTB_W4
+  if (elem == 8) v.push_back({4, 4});
+#endif
   // DTB_SHAPE=K,W pins one shape (experiments)
   if (const char* e = getenv("DTB_SHAPE")) {
     int k = 0, w = 0;
@@ -182,7 +190,7 @@ bool plan_resident(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInf
         for (int nty = nty_max; nty >= std::max(1, nty_max - 2); --nty) {
           Split sy;
           // (L - 2) a multiple of 4 rows per band: the static sweep fast path
-          if (!make_split((int)ny, nty, h, 4 * W, maxRows, nty > 1 ? h : 1, sy, 2)) continue;
+          if (!make_split((int)ny, nty, h, W <= 8 ? 4 * W : 4, maxRows, nty > 1 ? h : 1, sy, 2)) continue;
           // cost per epoch of hh steps: slowest CTA + exchange
           double cyc = tile_cycles(elem, K, W, sy.max_load, hh);
           if (steps > hh) {
@@ -328,8 +336,49 @@ bool plan_pipe(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& d
 
 }  // namespace
 
+static bool make_plan_search(int64_t nx, int64_t ny, int elem, int64_t steps,
+                             const DevInfo& dev, int force, int depth, Plan& out, char* err,
+                             int errlen);
+
+// The planner's search (depths x tile counts x shapes) costs ~0.5 ms of host
+// time; solves of the same shape reuse the last plans (small MRU cache).
 bool make_plan(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& dev, int force,
                int depth, Plan& out, char* err, int errlen) {
+  struct Key {
+    int64_t nx, ny, steps, smem_optin, l2, smem_sm;
+    int elem, force, depth, sms;
+    std::string shape;
+    bool operator==(const Key& o) const {
+      return nx == o.nx && ny == o.ny && steps == o.steps && smem_optin == o.smem_optin &&
+             l2 == o.l2 && smem_sm == o.smem_sm && elem == o.elem && force == o.force &&
+             depth == o.depth && sms == o.sms && shape == o.shape;
+    }
+  };
+  static std::mutex mu;
+  static std::vector<std::pair<Key, Plan>> cache;  // most recent first
+  const char* sh = getenv("DTB_SHAPE");
+  const Key key{nx, ny, steps, dev.smem_optin, dev.l2_bytes, dev.smem_per_sm,
+                elem, force, depth, dev.sms, sh ? sh : ""};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (size_t i = 0; i < cache.size(); ++i) {
+      if (cache[i].first == key) {
+        out = cache[i].second;
+        if (i) std::rotate(cache.begin(), cache.begin() + i, cache.begin() + i + 1);
+        return true;
+      }
+    }
+  }
+  if (!make_plan_search(nx, ny, elem, steps, dev, force, depth, out, err, errlen)) return false;
+  std::lock_guard<std::mutex> lk(mu);
+  cache.insert(cache.begin(), {key, out});
+  if (cache.size() > 32) cache.pop_back();
+  return true;
+}
+
+static bool make_plan_search(int64_t nx, int64_t ny, int elem, int64_t steps,
+                             const DevInfo& dev, int force, int depth, Plan& out, char* err,
+                             int errlen) {
   if (nx < 1 || ny < 1) {
     snprintf(err, errlen, "domain dims must be at least 1x1, got %lldx%lld", (long long)nx,
              (long long)ny);
