@@ -666,7 +666,14 @@ pipe_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int n
   constexpr int kRing0Rows = PipeCfg<NW>::kRing0Rows, kRingRows = PipeCfg<NW>::kRingRows;
   constexpr int kPipeBytes = (kRing0Rows + (S - 1) * kRingRows) * RB;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int warp = threadIdx.x >> 5, p = warp / S, s = warp % S;
+#ifndef DTB_PIPE_MAP
+#define DTB_PIPE_MAP 1
+#endif
+  // DTB_PIPE_MAP 1: warp = s * P + p, so SM sub-partition (warp % 4) p hosts all
+  // S stages of pipeline p and a stage's slack goes to its own upstream/downstream
+  // warps; 0: warp = p * S + s (all stage-0 warps share one sub-partition)
+  const int warp = threadIdx.x >> 5;
+  const int p = DTB_PIPE_MAP ? warp % P : warp / S, s = DTB_PIPE_MAP ? warp / P : warp % S;
   PipeSmem<S>* ctl = reinterpret_cast<PipeSmem<S>*>(smem_raw + P * kPipeBytes);
   if (threadIdx.x < P * S) {
     ctl[threadIdx.x / S].prod[threadIdx.x % S] = 0;

@@ -58,11 +58,17 @@ __device__ __forceinline__ void pipe_commit() { asm volatile("cp.async.commit_gr
 // per CTA width: 8 warps = 2 pipelines with deep rings, 16 warps = 4
 // pipelines with shallower rings (the smem budget). Block-level flow control
 // needs kRingRows >= 12 to stay deadlock-free (see pipe_stage).
+#ifndef DTB_PIPE_R0
+#define DTB_PIPE_R0 12
+#endif
+#ifndef DTB_PIPE_PF
+#define DTB_PIPE_PF 6
+#endif
 template <int NW>
 struct PipeCfg {
-  static constexpr int kRing0Rows = NW >= 16 ? 12 : 16;  // warp 0's HBM prefetch ring
+  static constexpr int kRing0Rows = NW >= 16 ? DTB_PIPE_R0 : 16;  // warp 0's HBM prefetch ring
   static constexpr int kRingRows = NW >= 16 ? 12 : 16;   // ring between consecutive warps
-  static constexpr int kPrefetch = NW >= 16 ? 6 : 8;     // HBM prefetch rows in flight
+  static constexpr int kPrefetch = NW >= 16 ? DTB_PIPE_PF : 8;     // HBM prefetch rows in flight
 };
 
 struct PipeTile {
@@ -77,12 +83,23 @@ struct PipeTile {
 // seq0: the pipeline-wide row sequence number of this tile's row 0 (ring
 // slot = seq % ring rows). `src` is read only by stage 0; `dst` written only
 // by the last stage.
-template <typename T, int K, int NW, bool DYN>
-__device__ __forceinline__ void pipe_stage(const PipeTile& pt, int stage, int nstages, int levels,
-                                           int seq0, const T* __restrict__ src,
-                                           T* __restrict__ dst, int64_t pitch, uint32_t ring_in,
-                                           uint32_t ring_out, int* prod, int* cons,
-                                           const Weights<T>& wt, const LaneCtx& lc) {
+// ROLE: 0 first stage (HBM prefetch in), 1 middle, 2 last stage (STG out);
+// resolved at compile time so the steady loop carries no role branches.
+#ifndef DTB_PIPE_NOINLINE
+#define DTB_PIPE_NOINLINE 0
+#endif
+#if DTB_PIPE_NOINLINE
+#define DTB_PIPE_INL __noinline__
+#else
+#define DTB_PIPE_INL __forceinline__
+#endif
+template <typename T, int K, int NW, bool DYN, int ROLE>
+__device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int levels,
+                                                int seq0, const T* __restrict__ src,
+                                                T* __restrict__ dst, int64_t pitch,
+                                                uint32_t ring_in, uint32_t ring_out, int* prod,
+                                                int* cons, const Weights<T>& wt,
+                                                const LaneCtx& lc, int nstages_) {
   typedef Tile<T, K> L;
   constexpr int E = L::EPC, CH = L::CH;
   constexpr uint32_t RB = (uint32_t)(L::ROW * sizeof(T));  // bytes per ring row
@@ -91,7 +108,11 @@ __device__ __forceinline__ void pipe_stage(const PipeTile& pt, int stage, int ns
   uint32_t off[CH];
 #pragma unroll
   for (int j = 0; j < CH; ++j) off[j] = (uint32_t)(L::swz(lane * CH + j) * 16);
-  const bool first = stage == 0, lastst = stage == nstages - 1;
+#ifndef DTB_PIPE_ROLES
+#define DTB_PIPE_ROLES 0  // 1: stage role as a template parameter (spills at 128 registers)
+#endif
+  const bool first = DTB_PIPE_ROLES ? ROLE == 0 : stage == 0;
+  const bool lastst = DTB_PIPE_ROLES ? ROLE == 2 : stage == nstages_ - 1;
   constexpr int kRing0Rows = PipeCfg<NW>::kRing0Rows, kRingRows = PipeCfg<NW>::kRingRows,
                 kPrefetch = PipeCfg<NW>::kPrefetch;
 
@@ -117,11 +138,23 @@ __device__ __forceinline__ void pipe_stage(const PipeTile& pt, int stage, int ns
   };
   // block-level flow control (steady loop): wait until rows [.., q_hi] are in
   // the input ring / ring slots up to output row q_hi are free
+#ifndef DTB_PIPE_ROW2
+// steady rows: 1 stage-major pair update, 0 two row updates (fp64 faster
+// with two, fp32 with the pair: B200 A/B, round 1)
+#define DTB_PIPE_ROW2 (sizeof(T) == 4)
+#endif
+#ifndef DTB_PIPE_POLL
+#define DTB_PIPE_POLL 1  // 1: every lane polls (warp-uniform loop); 0: lane 0 polls + syncwarp
+#endif
   auto wait_in = [&](int q_hi) {
     if (!first) {
-      if (lane == 0)
+      if (DTB_PIPE_POLL) {
         while (ld_acquire_cta(prod + stage) < seq0 + q_hi + 1) __nanosleep(20);
-      __syncwarp();
+      } else {
+        if (lane == 0)
+          while (ld_acquire_cta(prod + stage) < seq0 + q_hi + 1) __nanosleep(20);
+        __syncwarp();
+      }
     }
   };
   auto release_in = [&](int q_done) {  // input rows < q_done fully read
@@ -132,9 +165,13 @@ __device__ __forceinline__ void pipe_stage(const PipeTile& pt, int stage, int ns
   };
   auto wait_out = [&](int q_hi) {
     if (!lastst) {
-      if (lane == 0)
+      if (DTB_PIPE_POLL) {
         while (ld_acquire_cta(cons + stage + 1) < seq0 + q_hi - kRingRows + 1) __nanosleep(20);
-      __syncwarp();
+      } else {
+        if (lane == 0)
+          while (ld_acquire_cta(cons + stage + 1) < seq0 + q_hi - kRingRows + 1) __nanosleep(20);
+        __syncwarp();
+      }
     }
   };
   auto release_out = [&](int q_done) {  // output rows < q_done written
@@ -239,7 +276,12 @@ __device__ __forceinline__ void pipe_stage(const PipeTile& pt, int stage, int ns
 #define DTB_PIPE_STEADY(TM1, TC, TP1, TP2, BR, BM1, BM2, BM3)                     \
   {                                                                               \
     get_row_nosync(r + 2, TP2);                                                   \
-    row_update2<T, K, DYN>(TM1, TC, TP1, BR, BM3, BM2, BM1, o, wt, lc);           \
+    if (DTB_PIPE_ROW2) {                                                          \
+      row_update2<T, K, DYN>(TM1, TC, TP1, BR, BM3, BM2, BM1, o, wt, lc);         \
+    } else {                                                                      \
+      row_update<T, K, DYN>(TM1, TC, TP1, BR, wt, lc);                            \
+      row_update<T, K, DYN>(BM3, BM2, BM1, o, wt, lc);                            \
+    }                                                                             \
     put_row_nosync(r - 2, o);                                                     \
     ++r;                                                                          \
   }
@@ -279,6 +321,23 @@ __device__ __forceinline__ void pipe_stage(const PipeTile& pt, int stage, int ns
   }
   if (first) pipe_wait_group<0>();  // drain empty tail groups
   if (!first && lane == 0) st_release_cta(cons + stage, seq0 + Lh);  // whole tile consumed
+}
+
+template <typename T, int K, int NW, bool DYN>
+__device__ __forceinline__ void pipe_stage(const PipeTile& pt, int stage, int nstages, int levels,
+                                           int seq0, const T* __restrict__ src,
+                                           T* __restrict__ dst, int64_t pitch, uint32_t ring_in,
+                                           uint32_t ring_out, int* prod, int* cons,
+                                           const Weights<T>& wt, const LaneCtx& lc) {
+  if (DTB_PIPE_ROLES && stage == 0)
+    pipe_stage_role<T, K, NW, DYN, 0>(pt, stage, levels, seq0, src, dst, pitch, ring_in,
+                                      ring_out, prod, cons, wt, lc, nstages);
+  else if (DTB_PIPE_ROLES && stage == nstages - 1)
+    pipe_stage_role<T, K, NW, DYN, 2>(pt, stage, levels, seq0, src, dst, pitch, ring_in,
+                                      ring_out, prod, cons, wt, lc, nstages);
+  else
+    pipe_stage_role<T, K, NW, DYN, 1>(pt, stage, levels, seq0, src, dst, pitch, ring_in,
+                                      ring_out, prod, cons, wt, lc, nstages);
 }
 
 }  // namespace dtb

@@ -295,7 +295,10 @@ bool plan_streaming(int64_t nx, int64_t ny, int elem, int64_t steps, const DevIn
 // a few long segments so that there are about two pipelines' worth of
 // segments per SM.
 bool plan_pipe(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& dev, Plan& best) {
-  const int K = elem == 8 ? 4 : 8, W = 16, S = 4, P = W / S, h = 2 * S;
+#ifndef DTB_PIPE_WARPS
+#define DTB_PIPE_WARPS 16
+#endif
+  const int K = elem == 8 ? 4 : 8, W = DTB_PIPE_WARPS, S = 4, P = W / S, h = 2 * S;
   const int Lw_max = 32 * K;
   const int per = Lw_max - 2 * h;
   Split sx;
@@ -320,7 +323,8 @@ bool plan_pipe(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& d
   const int64_t ntiles = (int64_t)ntx * nseg;
   best.ctas = (int)std::min<int64_t>(dev.sms, (ntiles + P - 1) / P);
   best.ctas_per_sm = 1;
-  best.smem_bytes = (int64_t)(12 + (S - 1) * 12) * Lw_max * elem * P;
+  const int ring = W >= 16 ? 12 : 16;
+  best.smem_bytes = (int64_t)(ring + (S - 1) * ring) * Lw_max * elem * P;
   // cost: all lane-cells of every pass at ~70% of the FP issue rate + fill
   double lane_cells = 0;
   for (int i = 0; i < sx.n; ++i)
