@@ -1190,7 +1190,10 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
 template <typename T, int K, int PW, bool DYN>
 int launch_pipe(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch,
                 int nx, int ny, const Weights<T>& wt, int64_t steps, cudaStream_t st) {
-  constexpr int S = 4, P = PW / S;
+#ifndef DTB_PIPE_STAGES
+#define DTB_PIPE_STAGES 4
+#endif
+  constexpr int S = DTB_PIPE_STAGES, P = PW / S;
   auto kern = pipe_kernel<T, K, PW, S, DYN>;
   const int pipe_bytes = (PipeCfg<PW>::kRing0Rows + (S - 1) * PipeCfg<PW>::kRingRows) *
                          Tile<T, K>::ROW * (int)sizeof(T);

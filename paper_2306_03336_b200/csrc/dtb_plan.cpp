@@ -2,6 +2,9 @@
 #include "dtb_plan.h"
 
 #include <algorithm>
+#ifndef DTB_PIPE_STAGES
+#define DTB_PIPE_STAGES 4  // pipeline stage warps (2 steps each): h = 2 * stages
+#endif
 #include <mutex>
 #include <string>
 #include <cmath>
@@ -298,7 +301,7 @@ bool plan_pipe(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& d
 #ifndef DTB_PIPE_WARPS
 #define DTB_PIPE_WARPS 16
 #endif
-  const int K = elem == 8 ? 4 : 8, W = DTB_PIPE_WARPS, S = 4, P = W / S, h = 2 * S;
+  const int K = elem == 8 ? 4 : 8, W = DTB_PIPE_WARPS, S = DTB_PIPE_STAGES, P = W / S, h = 2 * S;
   const int Lw_max = 32 * K;
   const int per = Lw_max - 2 * h;
   Split sx;
@@ -411,7 +414,7 @@ static bool make_plan_search(int64_t nx, int64_t ny, int elem, int64_t steps,
     // streaming kernel on B200: 0.85 vs 0.64 Tcells/s fp64 at 16384^2), with
     // the tile sweep as the fallback (a forced depth other than 8, tiny grids)
     ok = plan_resident(nx, ny, elem, steps, dev, depth, p);
-    if (!ok && (depth == 0 || depth == 8) && nx >= 64 && ny >= 64)
+    if (!ok && (depth == 0 || depth == 2 * DTB_PIPE_STAGES) && nx >= 64 && ny >= 64)
       ok = plan_pipe(nx, ny, elem, steps, dev, p);
     if (!ok) ok = plan_streaming(nx, ny, elem, steps, dev, depth, p);
   }
