@@ -46,7 +46,7 @@ METRIC = "j2d5pt GCells/s (fp64/fp32) at 1/2/4/8 B200 vs roofline and CPU refere
 def measured_peaks():
     """Roofline denominators: HBM from MEASURED_PEAKS.json (driver-written);
     smem and FP64/FP32 issue rates from this repo's B200 microbenchmarks
-    (tools/microbench/peaks.cu, profiles/r01_microbench_peaks.log)."""
+    (tools/microbench/peaks.cu, profiles/r01/microbench_peaks.log)."""
     peaks = {"hbm_gbs": 6545.3, "hbm_src": "fallback"}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -74,7 +74,7 @@ def ncu_traffic(kernel, dtype):
     for name, rec in summ.items():
         if name.startswith(kernel + "<" + tag):
             return rec["dram_bytes_read"] + rec["dram_bytes_write"], \
-                f"{rec['capture']} ({rec['workload']}; per launch, GB-scale inputs stay L2-resident for C2)"
+                f"{rec['capture']} ({rec['workload']}; DRAM read + write per launch of that capture)"
     return None, None
 
 
@@ -389,9 +389,9 @@ def run_b200(args):
     fp_peak = peaks["fp64_gops"] if elem == 8 else peaks["fp32_gops"]
     rooflines = {
         "smem": {"achieved": cells_per_s * 2 * elem / 1e9, "peak": peaks["smem_gbs"], "unit": "GB/s",
-                 "bytes_per_cell": 2 * elem, "peak_src": "microbench LDS.128 (profiles/r01_microbench_peaks.log)"},
+                 "bytes_per_cell": 2 * elem, "peak_src": "microbench LDS.128 (profiles/r01/microbench_peaks.log)"},
         "fp_pipe": {"achieved": cells_per_s * 9 / 1e9, "peak": fp_peak, "unit": "Gop/s",
-                    "ops_per_cell": 9, "peak_src": "microbench DMUL/DADD (profiles/r01_microbench_peaks.log)"},
+                    "ops_per_cell": 9, "peak_src": "microbench DMUL/DADD (profiles/r01/microbench_peaks.log)"},
         "hbm": {"achieved": cells_per_s * 2 * elem / max(plan.halo, 1) / 1e9
                 if plan.mode in ("streaming", "pipe") else grid_bytes * 2 / kernel_s / 1e9,
                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "peak_src": peaks["hbm_src"]},
