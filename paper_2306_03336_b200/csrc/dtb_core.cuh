@@ -52,7 +52,9 @@
 #endif
 #ifndef DTB_RING
 #define DTB_RING 2      // resident halo refresh: 0 generic, 1 ring copy after one wait,
-                        // 2 warp per direction: poll that neighbour, then copy its region
+                        // 2 warp per direction: poll that neighbour, then copy its region,
+                        // 3 warp per band: per-warp flags, each warp refreshes its own
+                        // band's side columns (+ a share of the N/S rows)
 #endif
 
 namespace dtb {
@@ -330,7 +332,9 @@ struct Publisher {
   int64_t pitch;
   int own0, own1, top1, bot0;
   uint32_t full_mask, side_mask;
-  int* flag;        // mode 3: this CTA's epoch flag (per-warp release-add)
+  int* flag;        // mode 3: this CTA's epoch flag (per-warp release-add);
+                    // DTB_RING 3: this CTA's per-warp flags (flag[warp] = epoch)
+  int epoch_val;    // DTB_RING 3: the epoch this sweep completes
   // mode 2/3: publish the band's own rows [ya, yb) from smem (they are final once
   // the band's last sweep is done: no other warp writes them)
   // mode 6: side columns flattened across lanes (lane i -> element i of the
@@ -644,6 +648,21 @@ __device__ __forceinline__ void band_rows4(int Lh, int nb, int b, int& ya, int& 
   if (b == nb - 1) yb = Lh - 1;
 }
 
+// Band [ya, yb) of warp w in the LAST sweep of an h-step epoch (two-step
+// sweeps when h is even, else a closing one-step sweep), as advance_tile lays
+// it out; ya == yb for warps without a band.
+__device__ __forceinline__ void last_sweep_band(int Lh, int h, int nw, int w, int& ya, int& yb) {
+  const int rows = Lh - 2;
+  ya = yb = 0;
+  if (h >= 2 && rows >= 2 && (h & 1) == 0) {
+    const int nb2 = max(1, min(nw, rows / 2));
+    if (w < nb2) band_rows4(Lh, nb2, w, ya, yb);
+  } else {
+    const int nb1 = max(1, min(nw, rows));
+    if (w < nb1) band_rows(Lh, nb1, w, ya, yb);
+  }
+}
+
 // Advance the tile `steps` time steps in place. All threads of the CTA call.
 // With `pub` non-null the final sweep also publishes the owned band.
 template <typename T, int K, bool DYN>
@@ -684,7 +703,11 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
           // neighbours wait for nwarps bumps per epoch (no CTA barrier first)
           __syncwarp();
           if (lc.lane == 0)
-            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
+            if (DTB_RING == 3)
+              asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(pub->flag + warp),
+                           "r"(pub->epoch_val) : "memory");
+            else
+              asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
         }
       }
       __syncthreads();
@@ -707,7 +730,11 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
         } else {
           __syncwarp();
           if (lc.lane == 0)
-            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
+            if (DTB_RING == 3)
+              asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(pub->flag + warp),
+                           "r"(pub->epoch_val) : "memory");
+            else
+              asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
         }
       }
       __syncthreads();

@@ -489,6 +489,86 @@ __device__ __forceinline__ void refresh_stamped(T* tile, const uint64_t* __restr
   }
 }
 
+// DTB_RING 3: wait until every warp of neighbour tile `nb` whose last-sweep
+// band intersects its rows [r0, r1) has published epoch `epoch` (lanes poll
+// one producer warp each).
+__device__ __forceinline__ void wait_band_flags(const int* flags, int nb, int nw, int Lh_p, int h,
+                                                int r0, int r1, int epoch, int lane) {
+  if (lane < nw) {
+    int ya, yb;
+    last_sweep_band(Lh_p, h, nw, lane, ya, yb);
+    if (ya < yb && ya < r1 && yb > r0) {
+      const int* f = flags + nb * nw + lane;
+      // relaxed polls (no L1 invalidate per poll while other warps' cp.async
+      // are in flight), one acquire once the flag is seen
+      while (ld_relaxed_gpu(f) < epoch) __nanosleep(32);
+      (void)ld_acquire_gpu(f);
+    }
+  }
+  __syncwarp();
+}
+
+// DTB_RING 3 halo refresh: warp w copies the W/E side columns of its own band's
+// owned rows (from the W/E neighbours' same-numbered bands) and, split by rows
+// across the first / second half of the warps, the N / S halo rows including
+// the corners. Only the producing warps' flags are awaited.
+template <typename T, int K>
+__device__ __forceinline__ void refresh_by_band(T* tile, const T* __restrict__ g, int64_t pitch,
+                                                int gx0, int gy0, const int* flags, int epoch,
+                                                const Geometry& geo, int tx, int ty, int Lh, int h,
+                                                int ry0, int oy0, int oy1, int ry1, int rx0,
+                                                int ox0, int ox1, int rx1,
+                                                unsigned long long* mark) {
+  typedef Tile<T, K> L;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const bool vec = ((gx0 % L::EPC) == 0) && ((pitch % L::EPC) == 0);
+  const int ntx = geo.ntx, nty = geo.nty;
+  // (a) side columns of this warp's band rows
+  int ya, yb;
+  last_sweep_band(Lh, h, nw, warp, ya, yb);
+  const int r0 = max(ya, oy0), r1 = min(yb, oy1);
+  const bool west = r0 < r1 && tx > 0 && rx0 < ox0;
+  const bool east = r0 < r1 && tx + 1 < ntx && ox1 < rx1;
+  // (b) N rows [ry0, oy0) on warps [0, G), S rows [oy1, ry1) on warps [G, nw)
+  const int G = max(1, nw / 2);
+  const bool north = warp < G;
+  const int nyt = ty + (north ? -1 : 1);
+  const int j = north ? warp : warp - G, nj = north ? G : nw - G;
+  const int q0 = north ? ry0 : oy1, q1 = north ? oy0 : ry1;
+  const bool rows_task = nyt >= 0 && nyt < nty && q0 < q1 && j < nj && q0 + j < q1;
+  int Lh_p = 0, shift = 0;
+  if (rows_task) {
+    const int4 cyn = geo.row[nyt];
+    Lh_p = cyn.w - cyn.z;
+    shift = (geo.row[ty].z + 1) - (cyn.z + 1);  // my tile row -> theirs
+  }
+  // every wait first (an acquire after cp.async has been issued would wait
+  // for those loads), then every copy
+  if (west) wait_band_flags(flags, ty * ntx + tx - 1, nw, Lh, h, r0, r1, epoch, lane);
+  if (east) wait_band_flags(flags, ty * ntx + tx + 1, nw, Lh, h, r0, r1, epoch, lane);
+  if (rows_task) {
+    for (int dx = -1; dx <= 1; ++dx) {
+      const int nxt = tx + dx;
+      const int c0 = dx < 0 ? rx0 : (dx == 0 ? ox0 : ox1);
+      const int c1 = dx < 0 ? ox0 : (dx == 0 ? ox1 : rx1);
+      if (nxt < 0 || nxt >= ntx || c0 >= c1) continue;
+      wait_band_flags(flags, nyt * ntx + nxt, nw, Lh_p, h, q0 + j + shift, q1 + shift, epoch,
+                      lane);
+    }
+  }
+  if (mark) *mark = clock64();
+  if (west) warp_g2s_chunks<T, K>(sbase, g, pitch, gx0, gy0, r0, r1, rx0, ox0, vec, lane);
+  if (east) warp_g2s_chunks<T, K>(sbase, g, pitch, gx0, gy0, r0, r1, ox1, rx1, vec, lane);
+  if (rows_task) {
+    for (int r = q0 + j; r < q1; r += nj) {
+      const int c0 = tx > 0 ? rx0 : ox0, c1 = tx + 1 < ntx ? rx1 : ox1;
+      warp_g2s_chunks<T, K>(sbase, g, pitch, gx0, gy0, r, r + 1, c0, c1, vec, lane);
+    }
+  }
+  cp_async_wait_all();
+}
+
 // Resident publish of the owned band: rows [oy0, t1) and [b0, oy1) in full
 // (one warp per row, coalesced), and the side columns [ox0, c1), [c2, ox1) of
 // the rows in between (one thread per row).
@@ -769,6 +849,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     tc = now_;                                         \
   }
   // per-lane publish masks over the lane's K columns (tile coordinates)
+  const bool band_flags = DTB_RING == 3 && !poison && (DTB_PUBREG == 3 || DTB_PUBREG == 6);
   Publisher<T, K> pub;
   pub.pitch = pitch;
   pub.own0 = oy0;
@@ -777,7 +858,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
   pub.bot0 = oy1 - bb;
   pub.full_mask = 0;
   pub.side_mask = 0;
-  pub.flag = flags + blockIdx.x;
+  pub.flag = band_flags ? flags + blockIdx.x * (int)(blockDim.x >> 5) : flags + blockIdx.x;
   pub.cl0 = ox0;
   pub.wl = bl;
   pub.cr0 = max(ox1 - br, ox0 + bl);
@@ -785,8 +866,8 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
   // flag value that marks "epoch e published": e (CTA-level release) or
   // e * warps (mode 3: one release-add per warp)
   const bool stamped = DTB_XCHG == 1 && !poison;
-  const int flag_per_epoch =
-      ((DTB_PUBREG == 3 || DTB_PUBREG == 4 || DTB_PUBREG == 6) && !poison) ? (int)(blockDim.x >> 5) : 1;
+  const int flag_per_epoch = band_flags ? 0 :
+      (((DTB_PUBREG == 3 || DTB_PUBREG == 4 || DTB_PUBREG == 6) && !poison) ? (int)(blockDim.x >> 5) : 1);
   {
     const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -804,6 +885,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     T* xb = ((epoch + 1) & 1) ? xb1 : xb0;
     pub.x = (((epoch + 1) & 1) ? xs1 : xs0) + ((int64_t)gy0 * pitch + gx0) * Stamped<T>::WPV;
     pub.stamp = stamp0 + (uint32_t)(epoch + 1);
+    pub.epoch_val = epoch + 1;
     pub.g0 = xb + (int64_t)gy0 * pitch + gx0;
     pub.g = pub.g0 + (threadIdx.x & 31) * K;
     // 1. compute the epoch; its final sweep publishes the owned band from registers
@@ -843,13 +925,29 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
       publish_sides<T, K>(tile, xb, pitch, gx0, gy0, oy0 + bt, oy1 - bb, ox0, ox0 + bl,
                           max(ox1 - br, ox0 + bl), ox1);
     }
+#ifndef DTB_SKIPBAR
+#define DTB_SKIPBAR 0  // 1: skip the post-publish CTA barrier in per-warp release modes (f64 +0.5 %, f32 -4 %)
+#endif
 #ifndef DTB_FENCE
 #define DTB_FENCE 0  // 0: thread 0 st.release after the barrier; 1: every thread fences first;
                      // 9: no fence (timing experiments only - unsynchronised)
 #endif
     DTB_MARK(t_pst)
     if (DTB_FENCE == 1) __threadfence();
-    __syncthreads();
+    // per-warp release modes need no CTA barrier here: advance() closed with one
+    if (band_flags) {
+      // 2+3. per band: no CTA barrier before (advance() closed with one)
+      DTB_MARK(t_pbar)
+      unsigned long long t_w = tc;
+      refresh_by_band<T, K>(tile, xb, pitch, gx0, gy0, flags, epoch, geo, tx, ty, Lh, h, ry0,
+                            oy0, oy1, ry1, rx0, ox0, ox1, rx1, tracing ? &t_w : nullptr);
+      if (tracing) t_pub += t_w - tc;  // warp 0: flag waits
+      DTB_MARK(t_wait)
+      __syncthreads();
+      DTB_MARK(t_ref)
+      continue;
+    }
+    if (flag_per_epoch == 1 || DTB_SKIPBAR == 0) __syncthreads();
     DTB_MARK(t_pbar)
     if (threadIdx.x == 0 && flag_per_epoch == 1) {
       if (DTB_FENCE == 9) *(volatile int*)(flags + blockIdx.x) = epoch;
@@ -1094,7 +1192,7 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
       return fail(DTB_ECAPACITY, "resident plan needs %d co-resident CTAs, device holds %d",
                   p.ctas, per_sm * sms);
     void* scratch = nullptr;
-    const size_t flag_bytes = 256 + (size_t)p.ctas * sizeof(int);
+    const size_t flag_bytes = 256 + (size_t)p.ctas * NW * sizeof(int);
     const size_t trace_bytes = (size_t)p.ctas * 8 * sizeof(unsigned long long);
     {
       std::lock_guard<std::mutex> lk(g_mu);
@@ -1105,7 +1203,7 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
     T* xb0 = reinterpret_cast<T*>(scratch);
     T* xb1 = reinterpret_cast<T*>(reinterpret_cast<char*>(scratch) + grid_bytes);
     int* flags = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + 2 * grid_bytes);
-    CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)p.ctas * sizeof(int), st));
+    CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)p.ctas * NW * sizeof(int), st));
     unsigned long long* trace = nullptr;
     if (tracing) {
       trace = reinterpret_cast<unsigned long long*>(

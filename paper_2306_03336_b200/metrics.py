@@ -15,7 +15,9 @@ from dataclasses import dataclass
 from .grid import Rect
 from .planner import DEFAULT_ELEM_BYTES, tile_active_region
 
-__all__ = ["TrafficReport", "model_naive_traffic", "model_dtb_traffic"]
+__all__ = ["TrafficReport", "model_naive_traffic", "model_dtb_traffic", "RUN_CSV_COLUMNS",
+           "run_csv_header", "run_csv_row", "format_bytes", "presets_csv",
+           "sota_footprint_table", "sota_footprint_csv"]
 
 
 @dataclass(frozen=True)
@@ -84,3 +86,67 @@ def model_dtb_traffic(plan, total_steps: int, valid=None) -> TrafficReport:
     return TrafficReport(loads * blocks, stores * blocks, halo * blocks,
                          compute * blocks - useful, useful, plan.footprint_bytes,
                          plan.elem_bytes)
+
+
+# --- CSV rows of the harness (metrics.py:133-205 of the reference) ----------
+# One stable schema for `run` and `sweep` rows; absent values stay empty.
+RUN_CSV_COLUMNS = (
+    "status", "nx", "ny", "valid_x0", "valid_y0", "valid_nx", "valid_ny",
+    "t_depth", "total_steps", "device", "workers",
+    "scratchpad_bytes_per_worker", "threads", "ilp", "seed",
+    "weight_w", "weight_e", "weight_s", "weight_c", "weight_n",
+    "tiles", "tile_w", "tile_h", "footprint_bytes", "elem_bytes",
+    "global_load_cells", "global_store_cells", "halo_exchanged_cells",
+    "redundant_compute_cells", "useful_compute_cells", "scratchpad_peak_bytes",
+    "bit_equal", "max_abs_diff", "wall_time_s", "host_model_gflops",
+)
+
+# published scratchpad footprints the paper compares against
+SOTA_FOOTPRINTS = (("StencilGen", "4.32 MB"), ("AN5D", "0.864 MB"))
+
+
+def run_csv_header() -> str:
+    return ",".join(RUN_CSV_COLUMNS)
+
+
+def run_csv_row(record: dict) -> str:
+    unknown = set(record) - set(RUN_CSV_COLUMNS)
+    if unknown:
+        raise ValueError(f"unknown CSV fields: {sorted(unknown)}")
+
+    def cell(v) -> str:
+        if v is None:
+            return ""
+        if isinstance(v, bool):
+            return "true" if v else "false"
+        return str(v)
+
+    return ",".join(cell(record.get(c)) for c in RUN_CSV_COLUMNS)
+
+
+def format_bytes(n: int) -> str:
+    """KB below 1 MiB, MB with two decimals above (1 KB = 1024 B)."""
+    if n < 0:
+        raise ValueError(f"negative byte count {n}")
+    kb = n / 1024.0
+    return f"{kb:g} KB" if kb < 1024.0 else f"{kb / 1024.0:.2f} MB"
+
+
+def sota_footprint_table(device=None) -> list:
+    rows = list(SOTA_FOOTPRINTS)
+    if device is not None:
+        rows.append((f"dtb-{device.name}", format_bytes(device.total_bytes)))
+    return rows
+
+
+def sota_footprint_csv(device=None) -> str:
+    return "\n".join(["name,scratchpad"]
+                     + [f"{n},{v}" for n, v in sota_footprint_table(device)]) + "\n"
+
+
+def presets_csv(presets: dict) -> str:
+    lines = ["name,workers,scratchpad_bytes_per_worker,total_bytes,total"]
+    for name, dev in presets.items():
+        lines.append(f"{name},{dev.workers},{dev.scratchpad_bytes_per_worker},"
+                     f"{dev.total_bytes},{format_bytes(dev.total_bytes)}")
+    return "\n".join(lines) + "\n"

@@ -16,7 +16,9 @@ Two planners live here:
 
 from __future__ import annotations
 
+import configparser
 import ctypes
+import os
 from dataclasses import dataclass
 
 from .grid import Rect
@@ -24,7 +26,7 @@ from .grid import Rect
 __all__ = ["DEFAULT_ELEM_BYTES", "DeviceModel", "DeviceTile", "SubTile", "TilingPlan",
            "InfeasiblePlanError", "scratchpad_footprint", "plan_device_tiles",
            "partition_widths", "partition_subtiles", "tile_active_region", "B200Plan",
-           "plan_b200", "b200_device_model"]
+           "plan_b200", "b200_device_model", "load_presets"]
 
 DEFAULT_ELEM_BYTES = 8
 
@@ -69,10 +71,17 @@ class DeviceTile:
 
 @dataclass(frozen=True)
 class SubTile:
+    """One worker's column slice of a tile's load region (planner.py:91-112)."""
+
     owner: int
     cols: Rect
     stage_left: Rect | None
     stage_right: Rect | None
+
+    def to_dict(self) -> dict:
+        return {"owner": self.owner, "cols": self.cols.to_dict(),
+                "stage_left": self.stage_left.to_dict() if self.stage_left else None,
+                "stage_right": self.stage_right.to_dict() if self.stage_right else None}
 
 
 @dataclass(frozen=True)
@@ -92,7 +101,9 @@ class TilingPlan:
                            "scratchpad_bytes_per_worker":
                                self.device.scratchpad_bytes_per_worker},
                 "footprint_bytes": self.footprint_bytes,
-                "tiles": [t.to_dict() for t in self.tiles]}
+                "tiles": [dict(t.to_dict(), subtiles=[s.to_dict() for s in
+                                                      partition_subtiles(t, self.device)])
+                          for t in self.tiles]}
 
 
 def scratchpad_footprint(tile_load_dims, t_depth: int, elem_bytes: int, workers: int) -> int:
@@ -238,3 +249,18 @@ def b200_device_model(sms: int | None = None, smem: int | None = None) -> Device
         else:
             sms, smem = sms or 148, smem or 232448
     return DeviceModel("b200", sms, smem)
+
+
+# --- device presets (planner.py:291-313 of the reference) -------------------
+PRESETS_PATH = os.path.join(os.path.dirname(__file__), "presets.ini")
+
+
+def load_presets(path=None) -> dict:
+    """Device capacity presets from an INI file (sections with ``workers`` and
+    ``scratchpad_bytes_per_worker``); the shipped file includes ``b200``."""
+    parser = configparser.ConfigParser()
+    with open(PRESETS_PATH if path is None else path) as fh:
+        parser.read_file(fh)
+    return {name: DeviceModel(name, parser[name].getint("workers"),
+                              parser[name].getint("scratchpad_bytes_per_worker"))
+            for name in parser.sections()}
