@@ -1136,9 +1136,65 @@ int stamped_get(StampArena& a, size_t bytes, int64_t epochs, cudaStream_t st, ui
   return DTB_OK;
 }
 
+// Per-call host work is on the critical path of short solves (C1: ~0.1 ms per
+// solve), so device attributes, kernel smem attributes and occupancy are
+// queried once per device / kernel and cached.
+int query_dev_uncached(DevInfo& d, int dev);
 int query_dev(DevInfo& d) {
-  int dev = 0, v = 0;
+  static std::mutex mu;
+  static DevInfo cache[16];
+  static bool have[16] = {};
+  int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (!have[dev & 15]) {
+    int rc = query_dev_uncached(cache[dev & 15], dev);
+    if (rc) return rc;
+    have[dev & 15] = true;
+  }
+  d = cache[dev & 15];
+  return DTB_OK;
+}
+
+// cudaFuncSetAttribute(max dynamic smem) raised monotonically per (kernel,
+// device) — a kernel's attribute is the max any call needed — and occupancy
+// cached per (kernel, device, smem, threads)
+int prepare_kernel(const void* kern, int device, int smem, int threads, int* per_sm) {
+  struct A {
+    const void* k;
+    int dev, smem;
+  };
+  struct O {
+    const void* k;
+    int dev, smem, threads, per_sm;
+  };
+  static std::mutex mu;
+  static std::vector<A> attrs;
+  static std::vector<O> occ;
+  std::lock_guard<std::mutex> lk(mu);
+  A* a = nullptr;
+  for (A& e : attrs)
+    if (e.k == kern && e.dev == device) a = &e;
+  if (!a || a->smem < smem) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    if (a) a->smem = smem;
+    else attrs.push_back({kern, device, smem});
+  }
+  if (!per_sm) return DTB_OK;
+  for (const O& e : occ)
+    if (e.k == kern && e.dev == device && e.smem == smem && e.threads == threads) {
+      *per_sm = e.per_sm;
+      return DTB_OK;
+    }
+  int n = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem));
+  occ.push_back({kern, device, smem, threads, n});
+  *per_sm = n;
+  return DTB_OK;
+}
+
+int query_dev_uncached(DevInfo& d, int dev) {
+  int v = 0;
   CUDA_TRY(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
   d.sms = v;
   CUDA_TRY(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -1183,11 +1239,11 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
   CUDA_TRY(cudaGetDevice(&device));
   if (p.mode == 0) {
     auto kern = resident_kernel<T, K, NW, DYN>;
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int per_sm = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
-    int sms = 0;
-    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    if (int rc = prepare_kernel((const void*)kern, device, smem, threads, &per_sm)) return rc;
+    DevInfo di;
+    if (int rc = query_dev(di)) return rc;
+    const int sms = di.sms;
     if (per_sm < 1 || p.ctas > per_sm * sms)
       return fail(DTB_ECAPACITY, "resident plan needs %d co-resident CTAs, device holds %d",
                   p.ctas, per_sm * sms);
@@ -1242,8 +1298,8 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
   if (p.mode == 3) return DTB_EINFEASIBLE;  // handled by launch_pipe
   // streaming passes, ping-ponging dst between out and a scratch grid
   auto kern = stream_kernel<T, K, NW, DYN>;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                smem * p.ctas_per_sm));
+  if (int rc = prepare_kernel((const void*)kern, device, smem * p.ctas_per_sm, threads, nullptr))
+    return rc;
   const int64_t passes = (steps + p.h - 1) / p.h;
   T* tmp = nullptr;
   if (passes > 1) {
@@ -1296,9 +1352,9 @@ int launch_pipe(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int
   const int pipe_bytes = (PipeCfg<PW>::kRing0Rows + (S - 1) * PipeCfg<PW>::kRingRows) *
                          Tile<T, K>::ROW * (int)sizeof(T);
   const int psmem = P * pipe_bytes + (int)sizeof(PipeSmem<S>) * P;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem));
   int device;
   CUDA_TRY(cudaGetDevice(&device));
+  if (int rc = prepare_kernel((const void*)kern, device, psmem, PW * 32, nullptr)) return rc;
   const size_t grid_bytes = (size_t)(ny + 2) * pitch * sizeof(T);
   const int64_t passes = (steps + 2 * S - 1) / (2 * S);
   T* tmp = nullptr;
@@ -1310,9 +1366,9 @@ int launch_pipe(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int
     tmp = reinterpret_cast<T*>(scratch);
   }
   const int64_t ntiles = (int64_t)geo.ntx * geo.nty;
-  int sms = 0;
-  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  const int ctas = (int)std::min<int64_t>(sms, (ntiles + P - 1) / P);
+  DevInfo di;
+  if (int rc = query_dev(di)) return rc;
+  const int ctas = (int)std::min<int64_t>(di.sms, (ntiles + P - 1) / P);
   const T* src = d_in;
   int64_t done = 0;
   for (int64_t i = 0; i < passes; ++i) {
