@@ -263,6 +263,27 @@ __device__ __forceinline__ void copy_row(const T (&a)[K], T (&b)[K]) {
   for (int e = 0; e < K; ++e) b[e] = a[e];
 }
 
+// Thread groups: GT == 0 is the whole CTA; GT > 0 splits the CTA into
+// blockDim.x / GT independent groups of GT threads (the resident kernel's two
+// tiles per CTA), each with its own named barrier 1 + group.
+template <int GT>
+__device__ __forceinline__ int gt_tid() {
+  if constexpr (GT != 0) return (int)(threadIdx.x % GT);
+  else return (int)threadIdx.x;
+}
+template <int GT>
+__device__ __forceinline__ int gt_n() {
+  if constexpr (GT != 0) return GT;
+  else return (int)blockDim.x;
+}
+template <int GT>
+__device__ __forceinline__ void gt_sync() {
+  if constexpr (GT != 0)
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(threadIdx.x / GT)), "n"(GT) : "memory");
+  else
+    __syncthreads();
+}
+
 #ifndef DTB_XCHG
 #define DTB_XCHG 0  // resident exchange: 0 mirror grid + release/acquire epoch flags,
                     // 1 stamped words (every 8-byte word carries the epoch stamp in its
@@ -453,7 +474,7 @@ struct Publisher {
 // branch-free steady loop; the first three and the last few (frozen rows,
 // pre-read halo rows) run through the general iteration.
 // ---------------------------------------------------------------------------
-template <typename T, int K, bool DYN, bool PUB>
+template <typename T, int K, bool DYN, bool PUB, int GT = 0>
 __device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya, int yb,
                                        bool active, const Weights<T>& wt, const LaneCtx& lc,
                                        const Publisher<T, K>& pub) {
@@ -469,7 +490,7 @@ __device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya,
     load_row<T, K>(la, yb, h0);
     if (!bot_frozen) load_row<T, K>(la, yb + 1, h1);
   }
-  __syncthreads();  // every foreign row is now in registers; owned rows are ours
+  gt_sync<GT>();  // every foreign row is now in registers; owned rows are ours
   if (!active) return;
   load_row<T, K>(la, ya, t2);
 
@@ -588,7 +609,7 @@ __device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya,
 
 // One-step band sweep (odd step counts): rows [ya, yb) get t+1;
 // reads t rows [ya-1, yb+1). yb - ya >= 1.
-template <typename T, int K, bool DYN, bool PUB>
+template <typename T, int K, bool DYN, bool PUB, int GT = 0>
 __device__ __forceinline__ void sweep1(const LaneAddr<T, K>& la, int Lh, int ya, int yb,
                                        bool active, const Weights<T>& wt, const LaneCtx& lc,
                                        const Publisher<T, K>& pub) {
@@ -598,7 +619,7 @@ __device__ __forceinline__ void sweep1(const LaneAddr<T, K>& la, int Lh, int ya,
     load_row<T, K>(la, ya - 1, a0);
     load_row<T, K>(la, yb, h0);
   }
-  __syncthreads();
+  gt_sync<GT>();
   if (!active) return;
   load_row<T, K>(la, ya, a1);
   int r = ya;
@@ -665,11 +686,11 @@ __device__ __forceinline__ void last_sweep_band(int Lh, int h, int nw, int w, in
 
 // Advance the tile `steps` time steps in place. All threads of the CTA call.
 // With `pub` non-null the final sweep also publishes the owned band.
-template <typename T, int K, bool DYN>
+template <typename T, int K, bool DYN, int GT = 0>
 __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
                              const Weights<T>& wt, const Publisher<T, K>* pub = nullptr) {
-  const int warp = threadIdx.x >> 5;
-  const int nw = blockDim.x >> 5;
+  const int warp = gt_tid<GT>() >> 5;
+  const int nw = gt_n<GT>() >> 5;
   LaneCtx lc;
   lc.lane = threadIdx.x & 31;
   const LaneAddr<T, K> la(tile, lc.lane);
@@ -688,8 +709,8 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
     const bool act = warp < nb2;
     const bool band_pub = pub && ((DTB_PUBREG == 1 && pub->covers(ya, yb)) || DTB_PUBREG == 4);
     for (; s + 2 <= steps; s += 2) {
-      if (band_pub && s + 2 == steps) sweep2<T, K, DYN, true>(la, Lh, ya, yb, act, wt, lc, pb);
-      else sweep2<T, K, DYN, false>(la, Lh, ya, yb, act, wt, lc, pb);
+      if (band_pub && s + 2 == steps) sweep2<T, K, DYN, true, GT>(la, Lh, ya, yb, act, wt, lc, pb);
+      else sweep2<T, K, DYN, false, GT>(la, Lh, ya, yb, act, wt, lc, pb);
       if (DTB_PUBREG >= 2 && pub && s + 2 == steps) {
         if (act && DTB_PUBREG != 4) pub->put_band(la, ya, yb);  // rows final: publish now
         if (DTB_PUBREG == 5) {
@@ -710,7 +731,7 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
               asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
         }
       }
-      __syncthreads();
+      gt_sync<GT>();
     }
   }
   if (s < steps) {
@@ -719,8 +740,8 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
     band_rows(Lh, nb1, min(warp, nb1 - 1), ya, yb);
     const bool band_pub = pub && ((DTB_PUBREG == 1 && pub->covers(ya, yb)) || DTB_PUBREG == 4);
     for (; s < steps; ++s) {
-      if (band_pub && s + 1 == steps) sweep1<T, K, DYN, true>(la, Lh, ya, yb, warp < nb1, wt, lc, pb);
-      else sweep1<T, K, DYN, false>(la, Lh, ya, yb, warp < nb1, wt, lc, pb);
+      if (band_pub && s + 1 == steps) sweep1<T, K, DYN, true, GT>(la, Lh, ya, yb, warp < nb1, wt, lc, pb);
+      else sweep1<T, K, DYN, false, GT>(la, Lh, ya, yb, warp < nb1, wt, lc, pb);
       if (DTB_PUBREG >= 2 && pub && s + 1 == steps) {
         if (warp < nb1 && DTB_PUBREG != 4) pub->put_band(la, ya, yb);
         if (DTB_PUBREG == 5) {
@@ -737,7 +758,7 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
               asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
         }
       }
-      __syncthreads();
+      gt_sync<GT>();
     }
   }
 }

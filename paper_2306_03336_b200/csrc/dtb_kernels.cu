@@ -100,18 +100,18 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // asynchronous global->shared copies (LDGSTS): no registers are held, every
 // copy of the CTA is in flight at once, one L2/HBM latency covers the lot.
 // The caller must __syncthreads() afterwards.
-template <typename T, int K, int N>
+template <typename T, int K, int N, int GT = 0>
 __device__ __forceinline__ void g2s(T* tile, const T* __restrict__ g, int64_t pitch, int gx0,
                                     int gy0, const RectList<N>& rl) {
   typedef Tile<T, K> L;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
-  const int nt = blockDim.x;
+  const int nt = gt_n<GT>();
 #pragma unroll
   for (int j = 0; j < N; ++j) {
     const int n = rl.end[j] - (j ? rl.end[j - 1] : 0);
     const uint32_t w = (uint32_t)rl.w[j];
     const uint64_t m = rl.m[j];
-    for (int i = threadIdx.x; i < n; i += nt) {
+    for (int i = gt_tid<GT>(); i < n; i += nt) {
       const uint32_t q = (uint32_t)(((uint64_t)(uint32_t)i * m) >> 32);
       const int r = rl.r0[j] + (int)q, c = rl.c0[j] + (int)((uint32_t)i - q * w);
       cp_async(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)),
@@ -122,12 +122,12 @@ __device__ __forceinline__ void g2s(T* tile, const T* __restrict__ g, int64_t pi
 }
 
 // global (padded coords) <- tile cells of `rl`
-template <typename T, int K, int N>
+template <typename T, int K, int N, int GT = 0>
 __device__ __forceinline__ void s2g(const T* tile, T* __restrict__ g, int64_t pitch, int gx0,
                                     int gy0, const RectList<N>& rl) {
   typedef Tile<T, K> L;
-  const int nt = blockDim.x;
-  for (int i = threadIdx.x; i < rl.total(); i += nt) {
+  const int nt = gt_n<GT>();
+  for (int i = gt_tid<GT>(); i < rl.total(); i += nt) {
     int r, c;
     rl.locate(i, r, c);
     __stcg(g + (int64_t)(gy0 + r) * pitch + (gx0 + c), tile[L::at(r, c)]);
@@ -136,13 +136,13 @@ __device__ __forceinline__ void s2g(const T* tile, T* __restrict__ g, int64_t pi
 
 // Resident halo refresh: top/bottom ring rows one warp per row (coalesced),
 // side ring columns one thread per row; all as cp.async, one latency.
-template <typename T, int K>
+template <typename T, int K, int GT = 0>
 __device__ __forceinline__ void refresh_ring(T* tile, const T* __restrict__ g, int64_t pitch,
                                              int gx0, int gy0, int ry0, int oy0, int oy1, int ry1,
                                              int rx0, int ox0, int ox1, int rx1) {
   typedef Tile<T, K> L;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int warp = gt_tid<GT>() >> 5, lane = threadIdx.x & 31, nw = gt_n<GT>() >> 5;
   const int ntop = oy0 - ry0, nrows = ntop + (ry1 - oy1);
   for (int k = warp; k < nrows; k += nw) {
     const int r = k < ntop ? ry0 + k : oy1 + (k - ntop);
@@ -150,7 +150,7 @@ __device__ __forceinline__ void refresh_ring(T* tile, const T* __restrict__ g, i
     for (int c = rx0 + lane; c < rx1; c += 32)
       cp_async(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)), src + c);
   }
-  for (int r = oy0 + threadIdx.x; r < oy1; r += blockDim.x) {
+  for (int r = oy0 + gt_tid<GT>(); r < oy1; r += gt_n<GT>()) {
     const T* src = g + (int64_t)(gy0 + r) * pitch + gx0;
     for (int c = rx0; c < ox0; ++c) cp_async(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)), src + c);
     for (int c = ox1; c < rx1; ++c) cp_async(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)), src + c);
@@ -185,13 +185,13 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 
-template <typename T, int K>
+template <typename T, int K, int GT = 0>
 __device__ __forceinline__ void g2s_rows(T* tile, const T* __restrict__ g, int64_t pitch, int gx0,
                                          int gy0, int r0, int r1, int c0, int c1) {
   typedef Tile<T, K> L;
   constexpr int E = L::EPC;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int warp = gt_tid<GT>() >> 5, lane = threadIdx.x & 31, nw = gt_n<GT>() >> 5;
   const bool vec = ((gx0 % E) == 0) && ((pitch % E) == 0);
   const int q0 = c0 / E, q1 = (c1 + E - 1) / E;
   for (int r = r0 + warp; r < r1; r += nw) {
@@ -211,13 +211,13 @@ __device__ __forceinline__ void g2s_rows(T* tile, const T* __restrict__ g, int64
   }
 }
 
-template <typename T, int K>
+template <typename T, int K, int GT = 0>
 __device__ __forceinline__ void s2g_rows(const T* tile, T* __restrict__ g, int64_t pitch, int gx0,
                                          int gy0, int r0, int r1, int c0, int c1) {
   typedef Tile<T, K> L;
   typedef typename Arith<T>::vec_t V;
   constexpr int E = L::EPC;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int warp = gt_tid<GT>() >> 5, lane = threadIdx.x & 31, nw = gt_n<GT>() >> 5;
   const bool vec = ((gx0 % E) == 0) && ((pitch % E) == 0);
   const int q0 = c0 / E, q1 = (c1 + E - 1) / E;
   for (int r = r0 + warp; r < r1; r += nw) {
@@ -285,7 +285,7 @@ __device__ __forceinline__ void warp_g2s_chunks(uint32_t sbase, const T* __restr
 // one neighbour; a warp polls that neighbour's epoch flag and streams the
 // task's cells in with cp.async as soon as they are published, so the waits
 // and loads overlap across warps.
-template <typename T, int K>
+template <typename T, int K, int GT = 0>
 __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restrict__ g,
                                                      int64_t pitch, int gx0, int gy0,
                                                      const int* flags, int epoch, int ntx, int nty,
@@ -298,7 +298,7 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
 #endif
   constexpr int kSideParts = DTB_SIDE_PARTS;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int warp = gt_tid<GT>() >> 5, lane = threadIdx.x & 31, nw = gt_n<GT>() >> 5;
   const bool vec = ((gx0 % L::EPC) == 0) && ((pitch % L::EPC) == 0);
   const int side_rows = oy1 - oy0;
   int polled = -1;  // neighbour this warp last waited for
@@ -396,7 +396,7 @@ __device__ __forceinline__ void warp_refresh_stamped(uint32_t sbase, const uint6
 #ifndef DTB_STAMP_SENTINEL
 #define DTB_STAMP_SENTINEL 1
 #endif
-template <typename T, int K>
+template <typename T, int K, int GT = 0>
 __device__ __forceinline__ void refresh_stamped(T* tile, const uint64_t* __restrict__ x,
                                                 int64_t pitch, int gx0, int gy0, uint32_t stamp,
                                                 int ntx, int nty, int tx, int ty, int ry0,
@@ -431,7 +431,7 @@ __device__ __forceinline__ void refresh_stamped(T* tile, const uint64_t* __restr
 #if DTB_STAMP_SENTINEL
     // thread k first waits on one word of rectangle k (cheap polling); the
     // bulk loads below then mostly find their stamps on the first try
-    if (on && (int)threadIdx.x == 32 * k) {
+    if (on && gt_tid<GT>() == 32 * k) {
       StampedLoad w;
       const uint64_t* q = x + ((int64_t)(gy0 + r1 - 1) * pitch + gx0 + c1 - 1) * WPV;
       ld_stamped(q, w, T());
@@ -443,16 +443,16 @@ __device__ __forceinline__ void refresh_stamped(T* tile, const uint64_t* __restr
 #endif
   }
 #if DTB_STAMP_SENTINEL
-  __syncthreads();
+  gt_sync<GT>();
 #endif
   if (mark) *mark = clock64();
-  for (int base = threadIdx.x; base < total; base += blockDim.x * kBatch) {
+  for (int base = gt_tid<GT>(); base < total; base += gt_n<GT>() * kBatch) {
     StampedLoad v[kBatch];
     const uint64_t* src[kBatch];
     uint32_t dst[kBatch];
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
-      const int i = base + (int)blockDim.x * j;
+      const int i = base + gt_n<GT>() * j;
       int k = 0, st0 = 0;
 #pragma unroll
       for (int q = 0; q < 7; ++q)
@@ -471,7 +471,7 @@ __device__ __forceinline__ void refresh_stamped(T* tile, const uint64_t* __restr
     uint32_t pending = 0;
 #pragma unroll
     for (int j = 0; j < kBatch; ++j)
-      if (base + (int)blockDim.x * j < total) pending |= 1u << j;
+      if (base + gt_n<GT>() * j < total) pending |= 1u << j;
     while (true) {
 #pragma unroll
       for (int j = 0; j < kBatch; ++j) {
@@ -512,7 +512,7 @@ __device__ __forceinline__ void wait_band_flags(const int* flags, int nb, int nw
 // owned rows (from the W/E neighbours' same-numbered bands) and, split by rows
 // across the first / second half of the warps, the N / S halo rows including
 // the corners. Only the producing warps' flags are awaited.
-template <typename T, int K>
+template <typename T, int K, int GT = 0>
 __device__ __forceinline__ void refresh_by_band(T* tile, const T* __restrict__ g, int64_t pitch,
                                                 int gx0, int gy0, const int* flags, int epoch,
                                                 const Geometry& geo, int tx, int ty, int Lh, int h,
@@ -521,7 +521,7 @@ __device__ __forceinline__ void refresh_by_band(T* tile, const T* __restrict__ g
                                                 unsigned long long* mark) {
   typedef Tile<T, K> L;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int warp = gt_tid<GT>() >> 5, lane = threadIdx.x & 31, nw = gt_n<GT>() >> 5;
   const bool vec = ((gx0 % L::EPC) == 0) && ((pitch % L::EPC) == 0);
   const int ntx = geo.ntx, nty = geo.nty;
   // (a) side columns of this warp's band rows
@@ -543,20 +543,40 @@ __device__ __forceinline__ void refresh_by_band(T* tile, const T* __restrict__ g
     Lh_p = cyn.w - cyn.z;
     shift = (geo.row[ty].z + 1) - (cyn.z + 1);  // my tile row -> theirs
   }
-  // every wait first (an acquire after cp.async has been issued would wait
-  // for those loads), then every copy
-  if (west) wait_band_flags(flags, ty * ntx + tx - 1, nw, Lh, h, r0, r1, epoch, lane);
-  if (east) wait_band_flags(flags, ty * ntx + tx + 1, nw, Lh, h, r0, r1, epoch, lane);
-  if (rows_task) {
-    for (int dx = -1; dx <= 1; ++dx) {
-      const int nxt = tx + dx;
-      const int c0 = dx < 0 ? rx0 : (dx == 0 ? ox0 : ox1);
-      const int c1 = dx < 0 ? ox0 : (dx == 0 ? ox1 : rx1);
-      if (nxt < 0 || nxt >= ntx || c0 >= c1) continue;
-      wait_band_flags(flags, nyt * ntx + nxt, nw, Lh_p, h, q0 + j + shift, q1 + shift, epoch,
-                      lane);
+  // every wait first, all in parallel: lane c polls candidate c (neighbour k
+  // of W, E, NW, N, NE / SW, S, SE x producer warp w) when that warp's
+  // last-sweep band covers rows this warp copies from that neighbour
+#pragma unroll
+  for (int rep = 0; rep < 2; ++rep) {
+    const int c = lane + 32 * rep, k = c / nw, w = c % nw;
+    if (k < 5) {
+      int nbx = tx, nby = ty, lo = 0, hi = 0, lhp = Lh;
+      bool need = false;
+      if (k == 0 && west) { nbx = tx - 1; lo = r0; hi = r1; need = true; }
+      if (k == 1 && east) { nbx = tx + 1; lo = r0; hi = r1; need = true; }
+      if (k >= 2 && rows_task) {
+        const int dx = k - 3;
+        const int c0 = dx < 0 ? rx0 : (dx == 0 ? ox0 : ox1);
+        const int c1 = dx < 0 ? ox0 : (dx == 0 ? ox1 : rx1);
+        nbx = tx + dx;
+        nby = nyt;
+        lo = q0 + j + shift;
+        hi = q1 + shift;
+        lhp = Lh_p;
+        need = nbx >= 0 && nbx < ntx && c0 < c1;
+      }
+      if (need) {
+        int ya2, yb2;
+        last_sweep_band(lhp, h, nw, w, ya2, yb2);
+        if (ya2 < yb2 && ya2 < hi && yb2 > lo) {
+          const int* f = flags + (nby * ntx + nbx) * nw + w;
+          while (ld_relaxed_gpu(f) < epoch) __nanosleep(32);
+          (void)ld_acquire_gpu(f);
+        }
+      }
     }
   }
+  __syncwarp();
   if (mark) *mark = clock64();
   if (west) warp_g2s_chunks<T, K>(sbase, g, pitch, gx0, gy0, r0, r1, rx0, ox0, vec, lane);
   if (east) warp_g2s_chunks<T, K>(sbase, g, pitch, gx0, gy0, r0, r1, ox1, rx1, vec, lane);
@@ -572,13 +592,13 @@ __device__ __forceinline__ void refresh_by_band(T* tile, const T* __restrict__ g
 // Resident publish of the owned band: rows [oy0, t1) and [b0, oy1) in full
 // (one warp per row, coalesced), and the side columns [ox0, c1), [c2, ox1) of
 // the rows in between (one thread per row).
-template <typename T, int K>
+template <typename T, int K, int GT = 0>
 __device__ __forceinline__ void publish_band(const T* tile, T* __restrict__ g, int64_t pitch,
                                              int gx0, int gy0, int oy0, int t1, int b0, int oy1,
                                              int ox0, int c1, int c2, int ox1) {
   typedef Tile<T, K> L;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int warp = gt_tid<GT>() >> 5, lane = threadIdx.x & 31, nw = gt_n<GT>() >> 5;
   const int ntop = t1 - oy0, nrows = ntop + (oy1 - b0);
   for (int k = warp; k < nrows; k += nw) {
     const int r = k < ntop ? oy0 + k : b0 + (k - ntop);
@@ -591,7 +611,7 @@ __device__ __forceinline__ void publish_band(const T* tile, T* __restrict__ g, i
   const int wl = c1 - ox0, wr = ox1 - c2, nr = b0 - t1;
   const int nl = wl > 0 ? nr * wl : 0, ntot = nl + (wr > 0 ? nr * wr : 0);
   const uint32_t ml = wl > 0 ? (65535u + wl) / wl : 0, mr = wr > 0 ? (65535u + wr) / wr : 0;
-  for (int i = threadIdx.x; i < ntot; i += blockDim.x) {
+  for (int i = gt_tid<GT>(); i < ntot; i += gt_n<GT>()) {
     int r, c;
     if (i < nl) {
       const uint32_t q = ((uint32_t)i * ml) >> 16;
@@ -609,12 +629,12 @@ __device__ __forceinline__ void publish_band(const T* tile, T* __restrict__ g, i
 
 // Resident publish of the side columns [c0, c1) and [c2, c3) of rows [r0, r1):
 // one thread per row.
-template <typename T, int K>
+template <typename T, int K, int GT = 0>
 __device__ __forceinline__ void publish_sides(const T* tile, T* __restrict__ g, int64_t pitch,
                                               int gx0, int gy0, int r0, int r1, int c0, int c1,
                                               int c2, int c3) {
   typedef Tile<T, K> L;
-  for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+  for (int r = r0 + gt_tid<GT>(); r < r1; r += gt_n<GT>()) {
     T* dst = g + (int64_t)(gy0 + r) * pitch + gx0;
     for (int c = c0; c < c1; ++c) __stcg(dst + c, tile[L::at(r, c)]);
     for (int c = c2; c < c3; ++c) __stcg(dst + c, tile[L::at(r, c)]);
@@ -627,11 +647,11 @@ __device__ __forceinline__ void publish_sides(const T* tile, T* __restrict__ g, 
 // lane columns. A stale read anywhere then propagates NaN into the owned
 // cells and fails the bitwise comparison (the reference's poison mode,
 // engine.py:16-20,174-177).
-template <typename T, int K>
+template <typename T, int K, int GT = 0>
 __device__ void poison_rim(T* tile, int Lw, int Lh, int done, bool hl, bool hr, bool ht, bool hb) {
   typedef Tile<T, K> L;
   const T nanv = (T)NAN;
-  for (int i = threadIdx.x; i < Lh * L::ROW; i += blockDim.x) {
+  for (int i = gt_tid<GT>(); i < Lh * L::ROW; i += gt_n<GT>()) {
     const int r = i / L::ROW, c = i % L::ROW;
     bool p = c >= Lw;
     p |= hl && c < done;
@@ -642,19 +662,19 @@ __device__ void poison_rim(T* tile, int Lw, int Lh, int done, bool hl, bool hr, 
   }
 }
 
-template <typename T, int K, bool DYN>
+template <typename T, int K, bool DYN, int GT = 0>
 __device__ void advance(T* tile, int Lw, int Lh, int steps, const Weights<T>& wt, bool poison,
                         bool hl, bool hr, bool ht, bool hb,
                         const Publisher<T, K>* pub = nullptr) {
   if (!poison) {
-    advance_tile<T, K, DYN>(tile, Lw, Lh, steps, wt, pub);
+    advance_tile<T, K, DYN, GT>(tile, Lw, Lh, steps, wt, pub);
     return;
   }
   // poison mode: one step at a time, NaN the stale rim after each
   for (int s = 0; s < steps; ++s) {
-    advance_tile<T, K, DYN>(tile, Lw, Lh, 1, wt);
-    poison_rim<T, K>(tile, Lw, Lh, s + 1, hl, hr, ht, hb);
-    __syncthreads();
+    advance_tile<T, K, DYN, GT>(tile, Lw, Lh, 1, wt);
+    poison_rim<T, K, GT>(tile, Lw, Lh, s + 1, hl, hr, ht, hb);
+    gt_sync<GT>();
   }
 }
 
@@ -808,24 +828,33 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
   return v;
 }
 
-template <typename T, int K, int NW, bool DYN>
-__global__ void __launch_bounds__(NW * 32, 1)
+// G > 1: G independent tiles per CTA, NW warps each (own named barrier, own
+// flags and epochs), stacked in shared memory; a tile's halo wait overlaps
+// the other tiles' sweeps.
+template <typename T, int K, int NW, bool DYN, int G = 1>
+__global__ void __launch_bounds__(NW * 32 * G, 1)
 resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ xb0,
                 T* __restrict__ xb1, uint64_t* __restrict__ xs0, uint64_t* __restrict__ xs1,
                 uint32_t stamp0, int* __restrict__ flags, int64_t pitch, int nx, int ny,
                 Weights<T> wt, int64_t total_steps, int h, int poison,
                 unsigned long long* __restrict__ trace, const __grid_constant__ Geometry geo) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* tile = reinterpret_cast<T*>(smem_raw);
-  const int tx = blockIdx.x % geo.ntx, ty = blockIdx.x / geo.ntx;
+  constexpr int GT = G > 1 ? NW * 32 : 0;  // thread group = one tile
+  const int group = G > 1 ? (int)(threadIdx.x / (NW * 32)) : 0;
+  // tile (tx, ty); a CTA's G tiles are vertically adjacent (ty = G*cy + group)
+  const int tx = blockIdx.x % geo.ntx, ty = G * (blockIdx.x / geo.ntx) + group;
+  const int vcta = ty * geo.ntx + tx;
+  int row_off = 0;  // rows of this CTA's earlier tiles in shared memory
+  for (int g = 0; g < group; ++g) row_off += geo.row[ty - group + g].w - geo.row[ty - group + g].z;
+  T* tile = reinterpret_cast<T*>(smem_raw) + (size_t)row_off * Tile<T, K>::ROW;
   const int4 cx = geo.col[tx], cy = geo.row[ty];
   const int Lw = cx.w - cx.z, Lh = cy.w - cy.z;
   const int gx0 = cx.z + 1, gy0 = cy.z + 1;  // padded coords of tile (0,0)
   const bool hl = cx.z > -1, hr = cx.w < nx + 1, ht = cy.z > -1, hb = cy.w < ny + 1;
 
-  g2s_rows<T, K>(tile, in, pitch, gx0, gy0, 0, Lh, 0, Lw);
+  g2s_rows<T, K, GT>(tile, in, pitch, gx0, gy0, 0, Lh, 0, Lw);
   cp_async_wait_all();
-  __syncthreads();
+  gt_sync<GT>();
 
   // how deep each neighbour's load region reaches into my owned cells
   const int bl = tx > 0 ? max(0, geo.col[tx - 1].w - cx.x) : 0;
@@ -840,7 +869,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
   int64_t done = 0;
   int epoch = 0;
   unsigned long long t_comp = 0, t_pub = 0, t_wait = 0, t_ref = 0, t_pst = 0, t_pbar = 0, tc = 0;
-  const bool tracing = trace != nullptr && threadIdx.x == 0;
+  const bool tracing = trace != nullptr && gt_tid<GT>() == 0;
   if (tracing) tc = clock64();
 #define DTB_MARK(acc)                                  \
   if (tracing) {                                       \
@@ -858,7 +887,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
   pub.bot0 = oy1 - bb;
   pub.full_mask = 0;
   pub.side_mask = 0;
-  pub.flag = band_flags ? flags + blockIdx.x * (int)(blockDim.x >> 5) : flags + blockIdx.x;
+  pub.flag = band_flags ? flags + vcta * NW : flags + vcta;
   pub.cl0 = ox0;
   pub.wl = bl;
   pub.cr0 = max(ox1 - br, ox0 + bl);
@@ -867,7 +896,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
   // e * warps (mode 3: one release-add per warp)
   const bool stamped = DTB_XCHG == 1 && !poison;
   const int flag_per_epoch = band_flags ? 0 :
-      (((DTB_PUBREG == 3 || DTB_PUBREG == 4 || DTB_PUBREG == 6) && !poison) ? (int)(blockDim.x >> 5) : 1);
+      (((DTB_PUBREG == 3 || DTB_PUBREG == 4 || DTB_PUBREG == 6) && !poison) ? NW : 1);
   {
     const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -889,7 +918,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     pub.g0 = xb + (int64_t)gy0 * pitch + gx0;
     pub.g = pub.g0 + (threadIdx.x & 31) * K;
     // 1. compute the epoch; its final sweep publishes the owned band from registers
-    advance<T, K, DYN>(tile, Lw, Lh, steps, wt, poison != 0, hl, hr, ht, hb,
+    advance<T, K, DYN, GT>(tile, Lw, Lh, steps, wt, poison != 0, hl, hr, ht, hb,
                        (last || poison || !DTB_PUBREG) ? nullptr : &pub);
     done += steps;
     DTB_MARK(t_comp)
@@ -899,18 +928,18 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
       unsigned long long t_s = 0;
       // 2+3. stamped words: no barrier, fence or flag; each warp polls its
       // ring tasks' words and stores them as they arrive
-      refresh_stamped<T, K>(tile, (epoch & 1) ? xs1 : xs0, pitch, gx0, gy0,
+      refresh_stamped<T, K, GT>(tile, (epoch & 1) ? xs1 : xs0, pitch, gx0, gy0,
                             stamp0 + (uint32_t)epoch, geo.ntx, geo.nty, tx, ty, ry0, oy0, oy1,
                             ry1, rx0, ox0, ox1, rx1, tracing ? &t_s : nullptr);
       if (tracing) t_pst += t_s - tc;
       DTB_MARK(t_wait)
-      __syncthreads();
+      gt_sync<GT>();
       DTB_MARK(t_ref)
       continue;
     }
     if (!poison && DTB_PUBREG == 0) {
       const int t1 = min(oy0 + bt, oy1), b0 = max(oy1 - bb, t1);
-      publish_band<T, K>(tile, xb, pitch, gx0, gy0, oy0, t1, b0, oy1, ox0, ox0 + bl,
+      publish_band<T, K, GT>(tile, xb, pitch, gx0, gy0, oy0, t1, b0, oy1, ox0, ox0 + bl,
                          max(ox1 - br, ox0 + bl), ox1);
     } else if (poison) {
       // poison mode publishes through smem (its sweeps run one step at a time)
@@ -919,10 +948,10 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
       band.set(1, max(oy1 - bb, oy0 + bt), oy1, ox0, ox1);
       band.set(2, oy0 + bt, oy1 - bb, ox0, ox0 + bl);
       band.set(3, oy0 + bt, oy1 - bb, max(ox1 - br, ox0 + bl), ox1);
-      s2g<T, K>(tile, xb, pitch, gx0, gy0, band);
+      s2g<T, K, 4, GT>(tile, xb, pitch, gx0, gy0, band);
     } else if (DTB_PUBREG == 1) {
       // side columns of the owned rows between the top/bottom bands
-      publish_sides<T, K>(tile, xb, pitch, gx0, gy0, oy0 + bt, oy1 - bb, ox0, ox0 + bl,
+      publish_sides<T, K, GT>(tile, xb, pitch, gx0, gy0, oy0 + bt, oy1 - bb, ox0, ox0 + bl,
                           max(ox1 - br, ox0 + bl), ox1);
     }
 #ifndef DTB_SKIPBAR
@@ -939,19 +968,19 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
       // 2+3. per band: no CTA barrier before (advance() closed with one)
       DTB_MARK(t_pbar)
       unsigned long long t_w = tc;
-      refresh_by_band<T, K>(tile, xb, pitch, gx0, gy0, flags, epoch, geo, tx, ty, Lh, h, ry0,
+      refresh_by_band<T, K, GT>(tile, xb, pitch, gx0, gy0, flags, epoch, geo, tx, ty, Lh, h, ry0,
                             oy0, oy1, ry1, rx0, ox0, ox1, rx1, tracing ? &t_w : nullptr);
       if (tracing) t_pub += t_w - tc;  // warp 0: flag waits
       DTB_MARK(t_wait)
-      __syncthreads();
+      gt_sync<GT>();
       DTB_MARK(t_ref)
       continue;
     }
-    if (flag_per_epoch == 1 || DTB_SKIPBAR == 0) __syncthreads();
+    if (flag_per_epoch == 1 || DTB_SKIPBAR == 0) gt_sync<GT>();
     DTB_MARK(t_pbar)
-    if (threadIdx.x == 0 && flag_per_epoch == 1) {
-      if (DTB_FENCE == 9) *(volatile int*)(flags + blockIdx.x) = epoch;
-      else st_release(flags + blockIdx.x, epoch);
+    if (gt_tid<GT>() == 0 && flag_per_epoch == 1) {
+      if (DTB_FENCE == 9) *(volatile int*)(flags + vcta) = epoch;
+      else st_release(flags + vcta, epoch);
     }
     DTB_MARK(t_pub)
     if (DTB_RING == 2) {
@@ -959,7 +988,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
       // and immediately streams that region in (overlaps the 8 waits and loads)
       DTB_MARK(t_wait)
       unsigned long long t_poll = tc;
-      refresh_by_direction<T, K>(tile, xb, pitch, gx0, gy0, flags, epoch * flag_per_epoch,
+      refresh_by_direction<T, K, GT>(tile, xb, pitch, gx0, gy0, flags, epoch * flag_per_epoch,
                                  geo.ntx, geo.nty, tx, ty, ry0, oy0, oy1, ry1, rx0, ox0, ox1,
                                  rx1, tracing ? &t_poll : nullptr);
       if (tracing) {
@@ -968,41 +997,41 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
         t_pst += now_ - t_poll;  // warp 0: its loads
         tc = now_;
       }
-      __syncthreads();
+      gt_sync<GT>();
     } else {
     // 2. wait for the (up to 8) neighbours of this epoch
-    if (threadIdx.x < 9 && threadIdx.x != 4) {
-      const int dx = (int)threadIdx.x % 3 - 1, dy = (int)threadIdx.x / 3 - 1;
+    if (gt_tid<GT>() < 9 && gt_tid<GT>() != 4) {
+      const int dx = gt_tid<GT>() % 3 - 1, dy = gt_tid<GT>() / 3 - 1;
       const int nxt = tx + dx, nyt = ty + dy;
       if (nxt >= 0 && nxt < geo.ntx && nyt >= 0 && nyt < geo.nty) {
         const int* f = flags + nyt * geo.ntx + nxt;
         while (ld_acquire(f) < epoch * flag_per_epoch) __nanosleep(32);
       }
     }
-    __syncthreads();
+    gt_sync<GT>();
     DTB_MARK(t_wait)
     // 3. refresh the halo ring (load region minus owned, domain ghost excluded)
     if (DTB_RING) {
-      refresh_ring<T, K>(tile, xb, pitch, gx0, gy0, ry0, oy0, oy1, ry1, rx0, ox0, ox1, rx1);
+      refresh_ring<T, K, GT>(tile, xb, pitch, gx0, gy0, ry0, oy0, oy1, ry1, rx0, ox0, ox1, rx1);
     } else {
       RectList<4> ring;
       ring.set(0, ry0, oy0, rx0, rx1);
       ring.set(1, oy1, ry1, rx0, rx1);
       ring.set(2, oy0, oy1, rx0, ox0);
       ring.set(3, oy0, oy1, ox1, rx1);
-      g2s<T, K>(tile, xb, pitch, gx0, gy0, ring);
+      g2s<T, K, 4, GT>(tile, xb, pitch, gx0, gy0, ring);
     }
-    __syncthreads();
+    gt_sync<GT>();
     }
     DTB_MARK(t_ref)
   }
 #undef DTB_MARK
   if (tracing) {
-    unsigned long long* tr = trace + 8 * blockIdx.x;
+    unsigned long long* tr = trace + 8 * vcta;
     tr[0] = t_comp; tr[1] = t_pub; tr[2] = t_wait; tr[3] = t_ref; tr[4] = epoch;
     tr[5] = t_pst; tr[6] = t_pbar;
   }
-  s2g_rows<T, K>(tile, out, pitch, gx0, gy0, oy0 - !ht, oy1 + !hb, ox0 - !hl, ox1 + !hr);
+  s2g_rows<T, K, GT>(tile, out, pitch, gx0, gy0, oy0 - !ht, oy1 + !hb, ox0 - !hl, ox1 + !hr);
 }
 
 // ---------------------------------------------------------------------------
@@ -1225,12 +1254,13 @@ Weights<T> to_weights(const T w[5]) {
   return k;
 }
 
-template <typename T, int K, int NW, bool DYN>
+template <typename T, int K, int NW, bool DYN, int G = 1>
 int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_out,
                         int64_t pitch, int nx, int ny, const Weights<T>& wt,
                         int64_t steps, bool poison, cudaStream_t st) {
   const bool tracing = (g_flags & DTB_FLAG_TRACE) != 0;
-  const int threads = NW * 32;
+  const int threads = NW * 32 * (p.mode == 0 ? G : 1);
+  const int64_t tiles = (int64_t)p.ctas * (p.mode == 0 ? G : 1);
   const int smem = (int)p.smem_bytes;
   const int dev = 0;
   (void)dev;
@@ -1238,7 +1268,7 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
   int device;
   CUDA_TRY(cudaGetDevice(&device));
   if (p.mode == 0) {
-    auto kern = resident_kernel<T, K, NW, DYN>;
+    auto kern = resident_kernel<T, K, NW, DYN, G>;
     int per_sm = 0;
     if (int rc = prepare_kernel((const void*)kern, device, smem, threads, &per_sm)) return rc;
     DevInfo di;
@@ -1248,8 +1278,8 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
       return fail(DTB_ECAPACITY, "resident plan needs %d co-resident CTAs, device holds %d",
                   p.ctas, per_sm * sms);
     void* scratch = nullptr;
-    const size_t flag_bytes = 256 + (size_t)p.ctas * NW * sizeof(int);
-    const size_t trace_bytes = (size_t)p.ctas * 8 * sizeof(unsigned long long);
+    const size_t flag_bytes = 256 + (size_t)tiles * NW * sizeof(int);
+    const size_t trace_bytes = (size_t)tiles * 8 * sizeof(unsigned long long);
     {
       std::lock_guard<std::mutex> lk(g_mu);
       int rc = arena_get(g_scratch[device & 15], 2 * grid_bytes + flag_bytes + trace_bytes + 256,
@@ -1259,7 +1289,7 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
     T* xb0 = reinterpret_cast<T*>(scratch);
     T* xb1 = reinterpret_cast<T*>(reinterpret_cast<char*>(scratch) + grid_bytes);
     int* flags = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + 2 * grid_bytes);
-    CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)p.ctas * NW * sizeof(int), st));
+    CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)tiles * NW * sizeof(int), st));
     unsigned long long* trace = nullptr;
     if (tracing) {
       trace = reinterpret_cast<unsigned long long*>(
@@ -1288,7 +1318,7 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
     if (tracing) {
-      std::vector<unsigned long long> h_tr((size_t)p.ctas * 8);
+      std::vector<unsigned long long> h_tr((size_t)tiles * 8);
       CUDA_TRY(cudaMemcpyAsync(h_tr.data(), trace, trace_bytes, cudaMemcpyDeviceToHost, st));
       CUDA_TRY(cudaStreamSynchronize(st));
       g_trace.assign(h_tr.begin(), h_tr.end());
@@ -1383,12 +1413,12 @@ int launch_pipe(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int
   return DTB_OK;
 }
 
-template <typename T, int K, int NW>
+template <typename T, int K, int NW, int G = 1>
 int dispatch_dyn(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch,
                  int nx, int ny, const Weights<T>& wt, int64_t steps, bool poison,
                  cudaStream_t st) {
-  return p.dyn() ? launch_plan_kernels<T, K, NW, true>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st)
-                 : launch_plan_kernels<T, K, NW, false>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st);
+  return p.dyn() ? launch_plan_kernels<T, K, NW, true, G>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st)
+                 : launch_plan_kernels<T, K, NW, false, G>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st);
 }
 
 // kernel shapes compiled (must match the planner's candidates, dtb_plan.cpp)
@@ -1404,8 +1434,12 @@ int dispatch(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_
                    : launch_pipe<T, KK, DTB_PIPE_WARPS, false>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, st);
   }
 #define DTB_SHAPE(KK, WW)                                                                  \
-  if (p.K == KK && p.warps == WW)                                                          \
+  if (p.K == KK && p.warps == WW && p.groups == 1)                                         \
     return dispatch_dyn<T, KK, WW>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st);
+  // two 4-warp tiles per CTA (resident only)
+  if (p.mode == 0 && p.groups == 2 && p.warps == 4 && p.K == (sizeof(T) == 8 ? 4 : 8))
+    return dispatch_dyn<T, sizeof(T) == 8 ? 4 : 8, 4, 2>(p, geo, d_in, d_out, pitch, nx, ny, wt,
+                                                         steps, poison, st);
   if constexpr (sizeof(T) == 8) {
     DTB_SHAPE(4, 8)
 #ifdef DTB_W12

@@ -14,7 +14,7 @@
 namespace dtb {
 
 bool make_split(int N, int n, int h, int align, int maxL, int min_owned, Split& s, int off,
-                int start_align) {
+                int start_align, int spread) {
   s = Split();
   if (n < 1 || N < 1) return false;
   s.n = n;
@@ -30,7 +30,9 @@ bool make_split(int N, int n, int h, int align, int maxL, int min_owned, Split& 
   const long Lt = S / n, rem = S % n;
   int x = 0;
   for (int i = 0; i < n; ++i) {
-    long own = Lt + (i < rem ? 1 : 0) - left[i] - right[i];
+    // spread == 2: the +1 remainder rows go to even tiles first (CTA pairs)
+    const long rank = spread == 2 ? ((i & 1) ? (n + 1) / 2 + i / 2 : i / 2) : i;
+    long own = Lt + (rank < rem ? 1 : 0) - left[i] - right[i];
     if (own < std::max(1, min_owned)) return false;
     s.o0[i] = x;
     s.o1[i] = x + (int)own;
@@ -214,6 +216,58 @@ bool plan_resident(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInf
             best.ctas = ntx * nty;
             best.ctas_per_sm = 1;
             best.smem_bytes = (int64_t)sy.max_load * row_bytes;
+            best.cycles_per_step = per_step;
+            best.cells_per_clk = cpc;
+          }
+        }
+        if (sx.max_load < Lw_max / 2 && ntx > ntx_min) break;
+      }
+    }
+  }
+  // two tiles per CTA (4-warp groups, vertically adjacent, one named barrier
+  // each): a tile's exchange overlaps its partner's sweeps. DTB_GROUPS=2
+  // forces it, =1 disables it; by default it is taken when it fits.
+  const char* ge = getenv("DTB_GROUPS");
+  const int gmode = ge ? atoi(ge) : 1;  // default off until measured
+  if (gmode != 1) {
+    const int K = elem == 8 ? 4 : 8, W = 4;
+    const int Lw_max = 32 * K;
+    const int64_t row_bytes = (int64_t)Lw_max * elem;
+    const int pairRows = (int)(dev.smem_optin / row_bytes);
+    for (int h : depths_for(depth)) {
+      const int hh = (int)std::min<int64_t>(h, std::max<int64_t>(steps, 1));
+      if (steps <= hh || h % 2) continue;  // only pays with exchanges; two-step sweeps
+      const int ntx_min = (int)((nx + 2 + Lw_max - 1) / Lw_max);
+      for (int ntx = std::max(1, ntx_min); ntx <= std::min<int64_t>(dev.sms, nx); ++ntx) {
+        Split sx;
+        if (!make_split((int)nx, ntx, h, K, Lw_max, ntx > 1 ? h : 1, sx, 0, 16 / elem)) continue;
+        const int nty_max = (int)std::min<int64_t>(dev.sms / ntx, ny / 2);
+        for (int nty = nty_max; nty >= std::max(1, nty_max - 2); --nty) {
+          Split sy;
+          if (!make_split((int)ny, 2 * nty, h, 1, pairRows, h, sy, 0, 1, 2)) continue;
+          int pair_max = 0;
+          for (int c = 0; c < nty; ++c)
+            pair_max = std::max(pair_max, (sy.l1[2 * c] - sy.l0[2 * c]) +
+                                              (sy.l1[2 * c + 1] - sy.l0[2 * c + 1]));
+          if (pair_max > pairRows) continue;
+          // cost: both tiles' sweeps back to back, the exchange hidden
+          const double cyc = tile_cycles(elem, K, 2 * W, pair_max, hh) + 0.15 * kExchangeLatency;
+          const double per_step = cyc / hh;
+          const double cpc = (double)nx * ny / per_step;
+          if (gmode == 2 || !found || cpc > best.cells_per_clk) {
+            if (gmode == 2 && found && best.groups == 2 && cpc <= best.cells_per_clk) continue;
+            found = true;
+            best.mode = 0;
+            best.elem = elem;
+            best.K = K;
+            best.warps = W;
+            best.groups = 2;
+            best.h = h;
+            best.sx = sx;
+            best.sy = sy;
+            best.ctas = ntx * nty;
+            best.ctas_per_sm = 1;
+            best.smem_bytes = (int64_t)pair_max * row_bytes;
             best.cycles_per_step = per_step;
             best.cells_per_clk = cpc;
           }

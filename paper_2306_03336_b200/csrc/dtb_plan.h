@@ -49,6 +49,7 @@ struct Plan {
   Split sx, sy;
   int ctas = 0;
   int ctas_per_sm = 1;
+  int groups = 1;       // resident: tiles per CTA (vertically adjacent, one warp group each)
   int64_t smem_bytes = 0;
   double cycles_per_step = 0;  // cost model
   double cells_per_clk = 0;
@@ -65,7 +66,7 @@ struct Plan {
 // `start_align` > 1: interior boundaries are nudged so every load region
 // starts at a padded index divisible by it (16-byte aligned tile copies).
 bool make_split(int N, int n, int h, int align, int maxL, int min_owned, Split& s,
-                int off = 0, int start_align = 1);
+                int off = 0, int start_align = 1, int spread = 1);
 
 // Choose the execution plan. force: 0 auto, 1 streaming, 2 naive.
 // depth > 0 pins the halo depth.

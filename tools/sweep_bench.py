@@ -39,8 +39,8 @@ if __name__ == "__main__":
             j2d5pt_device(a, b, nx, ny, StencilWeights.diffusive(0.2), steps,
                           flags=flags | _native.FLAG_TRACE, depth=depth)
             torch.cuda.synchronize()
-            buf = (ctypes.c_int64 * (8 * 200))()
-            n = _native.lib().dtb_last_trace(buf, 8 * 200)
+            buf = (ctypes.c_int64 * (8 * 2048))()
+            n = min(2048, _native.lib().dtb_last_trace(buf, 8 * 2048))
             v = [list(buf[8 * i:8 * i + 8]) for i in range(n)]
             tot = [sum(x[k] for x in v) / max(n, 1) for k in range(8)]
             cyc = tot[0] + tot[1] + tot[2]
@@ -55,8 +55,8 @@ if __name__ == "__main__":
             j2d5pt_device(a, b, nx, ny, StencilWeights.diffusive(0.2), steps,
                           flags=flags | _native.FLAG_TRACE, depth=depth)
             torch.cuda.synchronize()
-            buf = (ctypes.c_int64 * (8 * 200))()
-            n = _native.lib().dtb_last_trace(buf, 8 * 200)
+            buf = (ctypes.c_int64 * (8 * 2048))()
+            n = min(2048, _native.lib().dtb_last_trace(buf, 8 * 2048))
             v = [list(buf[8 * i:8 * i + 8]) for i in range(n)]
             tot = [sum(x[k] for x in v) / n for k in range(8)]
             cyc = sum(tot[:4])
