@@ -143,16 +143,19 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
 // with two, fp32 with the pair: B200 A/B, round 1)
 #define DTB_PIPE_ROW2 (sizeof(T) == 4)
 #endif
+#ifndef DTB_PIPE_SLEEP
+#define DTB_PIPE_SLEEP 400  // ns between ring-counter polls (fp32 +2.5 %, fp64 flat vs 20)
+#endif
 #ifndef DTB_PIPE_POLL
 #define DTB_PIPE_POLL 1  // 1: every lane polls (warp-uniform loop); 0: lane 0 polls + syncwarp
 #endif
   auto wait_in = [&](int q_hi) {
     if (!first) {
       if (DTB_PIPE_POLL) {
-        while (ld_acquire_cta(prod + stage) < seq0 + q_hi + 1) __nanosleep(20);
+        while (ld_acquire_cta(prod + stage) < seq0 + q_hi + 1) __nanosleep(DTB_PIPE_SLEEP);
       } else {
         if (lane == 0)
-          while (ld_acquire_cta(prod + stage) < seq0 + q_hi + 1) __nanosleep(20);
+          while (ld_acquire_cta(prod + stage) < seq0 + q_hi + 1) __nanosleep(DTB_PIPE_SLEEP);
         __syncwarp();
       }
     }
@@ -166,10 +169,10 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
   auto wait_out = [&](int q_hi) {
     if (!lastst) {
       if (DTB_PIPE_POLL) {
-        while (ld_acquire_cta(cons + stage + 1) < seq0 + q_hi - kRingRows + 1) __nanosleep(20);
+        while (ld_acquire_cta(cons + stage + 1) < seq0 + q_hi - kRingRows + 1) __nanosleep(DTB_PIPE_SLEEP);
       } else {
         if (lane == 0)
-          while (ld_acquire_cta(cons + stage + 1) < seq0 + q_hi - kRingRows + 1) __nanosleep(20);
+          while (ld_acquire_cta(cons + stage + 1) < seq0 + q_hi - kRingRows + 1) __nanosleep(DTB_PIPE_SLEEP);
         __syncwarp();
       }
     }
