@@ -71,7 +71,9 @@ template <> struct Arith<float> {
   static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
 };
 
-template <typename T> struct Weights { T w, e, s, c, n; };
+// nz: -0.0 supplied at run time (see f2mul: an opaque zero addend keeps
+// ptxas from fusing a packed product into the following packed add)
+template <typename T> struct Weights { T w, e, s, c, n, nz; };
 
 // The reference's update for one cell, kernel.py:137-139 / grid.py:95-116.
 template <typename T>
@@ -182,6 +184,73 @@ struct LaneCtx {
   int last_e;  // its element index (== K-1 unless DYN)
 };
 
+// Packed FP32 (sm_100a fma/add.rn.f32x2): two cells per instruction, each
+// element rounded exactly like __fadd_rn/__fmul_rn (no fusion, no FTZ), so
+// results are bitwise those of the scalar expression. On B200 a packed
+// instruction issues at half rate, so the element rate equals scalar FP32
+// (tools/microbench/f32x2.cu); it only frees issue slots. Measured no gain
+// for the resident sweep and spills in the 128-register pipe: off by default.
+#ifndef DTB_F32X2
+#define DTB_F32X2 0  // off: same element rate as scalar FP32 on B200 (packed ops issue at half rate)
+#endif
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+// x*w rounded once, as fma(x, w, -0.0) with the -0.0 a kernel argument: ptxas
+// (12.9) contracts mul.rn.f32x2 + add.rn.f32x2 into one FFMA2 even with
+// --fmad=false, and folds fma(x, w, constant -0) the same way; an addend it
+// cannot see keeps the product and the sum separately rounded. fma(x, w, -0)
+// equals round(x*w) bit for bit (exact product + -0 is the exact product,
+// signed zeros included).
+__device__ __forceinline__ uint64_t f2mul(uint64_t a, uint64_t b, uint64_t nz) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(nz));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// cells (2p, 2p+1) of a row: ((((W*w + E*e) + S*s) + C*c) + N*n) per element
+__device__ __forceinline__ uint64_t f2cell(uint64_t W, uint64_t E, uint64_t S, uint64_t C,
+                                           uint64_t N, const uint64_t (&pw)[6]) {
+  uint64_t acc = f2mul(W, pw[0], pw[5]);
+  acc = f2add(acc, f2mul(E, pw[1], pw[5]));
+  acc = f2add(acc, f2mul(S, pw[2], pw[5]));
+  acc = f2add(acc, f2mul(C, pw[3], pw[5]));
+  acc = f2add(acc, f2mul(N, pw[4], pw[5]));
+  return acc;
+}
+template <int K>
+__device__ __forceinline__ void row_update_f32x2(const float (&up)[K], const float (&mid)[K],
+                                                 const float (&dn)[K], float (&out)[K],
+                                                 float west_edge, float east_edge,
+                                                 const uint64_t (&pw)[6]) {
+#pragma unroll
+  for (int p = 0; p < K / 2; ++p) {
+    const int e0 = 2 * p, e1 = 2 * p + 1;
+    const uint64_t W = f2pack(e0 == 0 ? west_edge : mid[e0 - 1], mid[e0]);
+    const uint64_t E = f2pack(mid[e1], e1 == K - 1 ? east_edge : mid[e1 + 1]);
+    const uint64_t acc = f2cell(W, E, f2pack(up[e0], up[e1]), f2pack(mid[e0], mid[e1]),
+                                f2pack(dn[e0], dn[e1]), pw);
+    f2unpack(acc, out[e0], out[e1]);
+  }
+}
+__device__ __forceinline__ void f2weights(const Weights<float>& wt, uint64_t (&pw)[6]) {
+  pw[0] = f2pack(wt.w, wt.w);
+  pw[1] = f2pack(wt.e, wt.e);
+  pw[2] = f2pack(wt.s, wt.s);
+  pw[3] = f2pack(wt.c, wt.c);
+  pw[4] = f2pack(wt.n, wt.n);
+  pw[5] = f2pack(wt.nz, wt.nz);
+}
+
 // One row of updates: out = stencil(up, mid, dn) for the lane's K columns;
 // frozen columns keep `mid`.
 template <typename T, int K, bool DYN>
@@ -189,11 +258,17 @@ __device__ __forceinline__ void row_update(const T (&up)[K], const T (&mid)[K], 
                                            T (&out)[K], const Weights<T>& wt, const LaneCtx& lc) {
   const T west_edge = shfl_up1(mid[K - 1]);
   const T east_edge = shfl_dn1(mid[0]);
+  if constexpr (sizeof(T) == 4 && K % 2 == 0 && DTB_F32X2) {
+    uint64_t pw[6];
+    f2weights(wt, pw);
+    row_update_f32x2<K>(up, mid, dn, out, west_edge, east_edge, pw);
+  } else {
 #pragma unroll
-  for (int e = 0; e < K; ++e) {
-    const T wv = (e == 0) ? west_edge : mid[e - 1];
-    const T ev = (e == K - 1) ? east_edge : mid[e + 1];
-    out[e] = cell_update(wv, ev, up[e], mid[e], dn[e], wt);
+    for (int e = 0; e < K; ++e) {
+      const T wv = (e == 0) ? west_edge : mid[e - 1];
+      const T ev = (e == K - 1) ? east_edge : mid[e + 1];
+      out[e] = cell_update(wv, ev, up[e], mid[e], dn[e], wt);
+    }
   }
   if (lc.first) out[0] = mid[0];
   if (DYN) {
@@ -220,6 +295,12 @@ __device__ __forceinline__ void row_update2(const T (&ua)[K], const T (&ma)[K], 
   typedef Arith<T> A;
   const T wa = shfl_up1(ma[K - 1]), ea = shfl_dn1(ma[0]);
   const T wb = shfl_up1(mb[K - 1]), eb = shfl_dn1(mb[0]);
+  if constexpr (sizeof(T) == 4 && K % 2 == 0 && DTB_F32X2) {
+    uint64_t pw[6];
+    f2weights(wt, pw);
+    row_update_f32x2<K>(ua, ma, da, oa, wa, ea, pw);
+    row_update_f32x2<K>(ub, mb, db, ob, wb, eb, pw);
+  } else {
 #pragma unroll
   for (int e = 0; e < K; ++e) {
     oa[e] = A::mul((e == 0) ? wa : ma[e - 1], wt.w);
@@ -244,6 +325,7 @@ __device__ __forceinline__ void row_update2(const T (&ua)[K], const T (&ma)[K], 
   for (int e = 0; e < K; ++e) {
     oa[e] = A::add(oa[e], A::mul(da[e], wt.n));
     ob[e] = A::add(ob[e], A::mul(db[e], wt.n));
+  }
   }
   if (lc.first) { oa[0] = ma[0]; ob[0] = mb[0]; }
   if (DYN) {

@@ -1251,6 +1251,7 @@ template <typename T>
 Weights<T> to_weights(const T w[5]) {
   Weights<T> k;
   k.w = w[0]; k.e = w[1]; k.s = w[2]; k.c = w[3]; k.n = w[4];
+  k.nz = (T)-0.0;
   return k;
 }
 
