@@ -345,6 +345,42 @@ __device__ __forceinline__ void copy_row(const T (&a)[K], T (&b)[K]) {
   for (int e = 0; e < K; ++e) b[e] = a[e];
 }
 
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];"
+               : "=r"(v)
+               : "r"((uint32_t)__cvta_generic_to_shared(p))
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)),
+               "r"(v)
+               : "memory");
+}
+
+// Band-to-band synchronisation of the two-step sweeps without CTA barriers
+// (DTB_BANDSYNC): per-warp counters in shared memory. pre[w] = the sweep whose
+// foreign rows warp w has read, done[w] = the last sweep warp w finished.
+// A warp reads its neighbours' seam rows once they are done with the previous
+// sweep, and overwrites its own seam rows only after the neighbour that reads
+// them has; warps never wait for the whole CTA, so one band's prologue or
+// epilogue overlaps the other bands' steady rows.
+struct BandSync {
+  int* pre;
+  int* done;
+  int seq;   // this sweep's number (1, 2, ...)
+  int nb;    // active bands
+};
+__device__ __forceinline__ void bs_wait(const int* p, int v) {
+  while (ld_acquire_cta(p) < v) {
+  }
+}
+__device__ __forceinline__ void bs_post(int* p, int v) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) st_release_cta(p, v);
+}
+
 // Thread groups: GT == 0 is the whole CTA; GT > 0 splits the CTA into
 // blockDim.x / GT independent groups of GT threads (the resident kernel's two
 // tiles per CTA), each with its own named barrier 1 + group.
@@ -559,21 +595,31 @@ struct Publisher {
 template <typename T, int K, bool DYN, bool PUB, int GT = 0>
 __device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya, int yb,
                                        bool active, const Weights<T>& wt, const LaneCtx& lc,
-                                       const Publisher<T, K>& pub) {
+                                       const Publisher<T, K>& pub,
+                                       const BandSync* bs = nullptr, int warp = 0) {
   T t0[K], t1[K], t2[K], t3[K];  // t rows
   T b0[K], b1[K], b2[K], b3[K];  // t+1 rows
   T h0[K], h1[K];                // pre-read bottom halo (t rows yb, yb+1)
   T o[K];
   const bool top_frozen = (ya == 1);       // row ya-1 is the frozen frame
   const bool bot_frozen = (yb == Lh - 1);  // row yb is the frozen frame
+  if (bs && active) {  // the neighbours' seam rows are final
+    if (warp > 0) bs_wait(bs->done + warp - 1, bs->seq - 1);
+    if (warp + 1 < bs->nb) bs_wait(bs->done + warp + 1, bs->seq - 1);
+  }
   if (active) {
     if (!top_frozen) load_row<T, K>(la, ya - 2, t0);
     load_row<T, K>(la, ya - 1, t1);
     load_row<T, K>(la, yb, h0);
     if (!bot_frozen) load_row<T, K>(la, yb + 1, h1);
   }
-  gt_sync<GT>();  // every foreign row is now in registers; owned rows are ours
-  if (!active) return;
+  if (bs) {
+    if (!active) return;
+    bs_post(bs->pre + warp, bs->seq);
+  } else {
+    gt_sync<GT>();  // every foreign row is now in registers; owned rows are ours
+    if (!active) return;
+  }
   load_row<T, K>(la, ya, t2);
 
   constexpr uint32_t kRowBytes = (uint32_t)(Tile<T, K>::ROW * sizeof(T));
@@ -606,6 +652,7 @@ __device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya,
     load_row<T, K>(la, ya + 3, t1);
     row_update<T, K, DYN>(t2, t3, t0, b2, wt, lc);
     // steady j=3 .. H-2 (r = ya+2 .. yb-3), (H-4)/4 blocks
+    if (bs && warp > 0) bs_wait(bs->pre + warp - 1, bs->seq);  // rows ya, ya+1 read
     uint32_t rowp = la.row(ya + 2);
     int rr = ya + 2;
     for (int blk = (H - 4) >> 2; blk > 0; --blk) {
@@ -615,6 +662,7 @@ __device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya,
       DTB_STEADY(t2, t3, t0, t1, b2, b1, b0, b3)
     }
     // tail j=H-1 (r=yb-2): t(yb) is h0; L1(yb-2), L2(yb-4)
+    if (bs && warp + 1 < bs->nb) bs_wait(bs->pre + warp + 1, bs->seq);  // rows yb-2, yb-1 read
     row_update2<T, K, DYN>(t3, t0, t1, b3, b0, b1, b2, o, wt, lc);
     store_row<T, K>(la, yb - 4, o);
     if (PUB) pub.put(yb - 4, o);
@@ -635,6 +683,7 @@ __device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya,
     row_update<T, K, DYN>(b3, b0, b1, o, wt, lc);
     store_row<T, K>(la, yb - 1, o);
     if (PUB) pub.put(yb - 1, o);
+    if (bs) bs_post(bs->done + warp, bs->seq);
     return;
   }
   // general iteration (any r): sources and frozen rows resolved by branches
@@ -661,6 +710,10 @@ __device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya,
   //   j%4==0: (t0,t1,t2,t3, b0,b3,b2,b1)   j%4==1: (t1,t2,t3,t0, b1,b0,b3,b2)
   //   j%4==2: (t2,t3,t0,t1, b2,b1,b0,b3)   j%4==3: (t3,t0,t1,t2, b3,b2,b1,b0)
   // ---- general path (any band height >= 2) ----
+  if (bs) {  // conservative: both seam neighbours have read before any store
+    if (warp > 0) bs_wait(bs->pre + warp - 1, bs->seq);
+    if (warp + 1 < bs->nb) bs_wait(bs->pre + warp + 1, bs->seq);
+  }
   int r = ya - 1;
   DTB_GEN(t0, t1, t2, t3, b0, b3, b2, b1)  // j = 0
   DTB_GEN(t1, t2, t3, t0, b1, b0, b3, b2)  // j = 1
@@ -685,6 +738,7 @@ __device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya,
     if (r > yb + 1) break;
     DTB_GEN(t2, t3, t0, t1, b2, b1, b0, b3)
   }
+  if (bs) bs_post(bs->done + warp, bs->seq);
 #undef DTB_GEN
 #undef DTB_STEADY
 }
@@ -770,7 +824,8 @@ __device__ __forceinline__ void last_sweep_band(int Lh, int h, int nw, int w, in
 // With `pub` non-null the final sweep also publishes the owned band.
 template <typename T, int K, bool DYN, int GT = 0>
 __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
-                             const Weights<T>& wt, const Publisher<T, K>* pub = nullptr) {
+                             const Weights<T>& wt, const Publisher<T, K>* pub = nullptr,
+                             int* bsmem = nullptr, int* bseq = nullptr) {
   const int warp = gt_tid<GT>() >> 5;
   const int nw = gt_n<GT>() >> 5;
   LaneCtx lc;
@@ -790,9 +845,18 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
     band_rows4(Lh, nb2, min(warp, nb2 - 1), ya, yb);
     const bool act = warp < nb2;
     const bool band_pub = pub && ((DTB_PUBREG == 1 && pub->covers(ya, yb)) || DTB_PUBREG == 4);
+    // band-to-band counters instead of CTA barriers between and inside the
+    // two-step sweeps (not with in-sweep publishing); one barrier closes the run
+    const bool use_bs = bsmem != nullptr && bseq != nullptr && !band_pub;
+    BandSync bsync;
+    bsync.pre = bsmem;
+    bsync.done = bsmem + nw;
+    bsync.nb = nb2;
     for (; s + 2 <= steps; s += 2) {
+      bsync.seq = use_bs ? ++*bseq : 0;
       if (band_pub && s + 2 == steps) sweep2<T, K, DYN, true, GT>(la, Lh, ya, yb, act, wt, lc, pb);
-      else sweep2<T, K, DYN, false, GT>(la, Lh, ya, yb, act, wt, lc, pb);
+      else sweep2<T, K, DYN, false, GT>(la, Lh, ya, yb, act, wt, lc, pb,
+                                        use_bs ? &bsync : nullptr, warp);
       if (DTB_PUBREG >= 2 && pub && s + 2 == steps) {
         if (act && DTB_PUBREG != 4) pub->put_band(la, ya, yb);  // rows final: publish now
         if (DTB_PUBREG == 5) {
@@ -813,7 +877,7 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
               asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
         }
       }
-      gt_sync<GT>();
+      if (!use_bs || s + 4 > steps) gt_sync<GT>();
     }
   }
   if (s < steps) {

@@ -665,9 +665,10 @@ __device__ void poison_rim(T* tile, int Lw, int Lh, int done, bool hl, bool hr, 
 template <typename T, int K, bool DYN, int GT = 0>
 __device__ void advance(T* tile, int Lw, int Lh, int steps, const Weights<T>& wt, bool poison,
                         bool hl, bool hr, bool ht, bool hb,
-                        const Publisher<T, K>* pub = nullptr) {
+                        const Publisher<T, K>* pub = nullptr, int* bsmem = nullptr,
+                        int* bseq = nullptr) {
   if (!poison) {
-    advance_tile<T, K, DYN, GT>(tile, Lw, Lh, steps, wt, pub);
+    advance_tile<T, K, DYN, GT>(tile, Lw, Lh, steps, wt, pub, bsmem, bseq);
     return;
   }
   // poison mode: one step at a time, NaN the stale rim after each
@@ -836,7 +837,7 @@ __global__ void __launch_bounds__(NW * 32 * G, 1)
 resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ xb0,
                 T* __restrict__ xb1, uint64_t* __restrict__ xs0, uint64_t* __restrict__ xs1,
                 uint32_t stamp0, int* __restrict__ flags, int64_t pitch, int nx, int ny,
-                Weights<T> wt, int64_t total_steps, int h, int poison,
+                Weights<T> wt, int64_t total_steps, int h, int poison, int bs_on,
                 unsigned long long* __restrict__ trace, const __grid_constant__ Geometry geo) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int GT = G > 1 ? NW * 32 : 0;  // thread group = one tile
@@ -852,6 +853,16 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
   const int gx0 = cx.z + 1, gy0 = cy.z + 1;  // padded coords of tile (0,0)
   const bool hl = cx.z > -1, hr = cx.w < nx + 1, ht = cy.z > -1, hb = cy.w < ny + 1;
 
+  // band-sync counters (DTB_BANDSYNC) after all of the CTA's tiles
+  int* bsmem = nullptr;
+  int bseq = 0;
+  if (bs_on) {
+    int rows_all = 0;
+    for (int g = 0; g < G; ++g) rows_all += geo.row[ty - group + g].w - geo.row[ty - group + g].z;
+    bsmem = reinterpret_cast<int*>(smem_raw + (size_t)rows_all * Tile<T, K>::ROW * sizeof(T)) +
+            group * 2 * NW;
+    if (gt_tid<GT>() < 2 * NW) bsmem[gt_tid<GT>()] = 0;
+  }
   g2s_rows<T, K, GT>(tile, in, pitch, gx0, gy0, 0, Lh, 0, Lw);
   cp_async_wait_all();
   gt_sync<GT>();
@@ -919,7 +930,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     pub.g = pub.g0 + (threadIdx.x & 31) * K;
     // 1. compute the epoch; its final sweep publishes the owned band from registers
     advance<T, K, DYN, GT>(tile, Lw, Lh, steps, wt, poison != 0, hl, hr, ht, hb,
-                       (last || poison || !DTB_PUBREG) ? nullptr : &pub);
+                           (last || poison || !DTB_PUBREG) ? nullptr : &pub, bsmem, &bseq);
     done += steps;
     DTB_MARK(t_comp)
     if (last) break;
@@ -1270,10 +1281,17 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
   CUDA_TRY(cudaGetDevice(&device));
   if (p.mode == 0) {
     auto kern = resident_kernel<T, K, NW, DYN, G>;
-    int per_sm = 0;
-    if (int rc = prepare_kernel((const void*)kern, device, smem, threads, &per_sm)) return rc;
     DevInfo di;
     if (int rc = query_dev(di)) return rc;
+#ifndef DTB_BANDSYNC
+#define DTB_BANDSYNC 0  // 1: band-to-band counters instead of CTA barriers inside an epoch (measured -1 %)
+#endif
+    // the band counters live after the tiles when the 1 KB of slack allows
+    const int bs_bytes = 2 * NW * G * (int)sizeof(int);
+    int bs_on = (DTB_BANDSYNC && !poison && smem + bs_bytes <= di.smem_optin) ? 1 : 0;
+    const int smem_res = smem + (bs_on ? bs_bytes : 0);
+    int per_sm = 0;
+    if (int rc = prepare_kernel((const void*)kern, device, smem_res, threads, &per_sm)) return rc;
     const int sms = di.sms;
     if (per_sm < 1 || p.ctas > per_sm * sms)
       return fail(DTB_ECAPACITY, "resident plan needs %d co-resident CTAs, device holds %d",
@@ -1313,9 +1331,9 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
     void* args[] = {(void*)&d_in, (void*)&d_out, (void*)&xb0, (void*)&xb1, (void*)&xs0,
                     (void*)&xs1, (void*)&stamp0, (void*)&flags,
                     (void*)&pitch, (void*)&nx, (void*)&ny, (void*)&wt, (void*)&steps,
-                    (void*)&h, (void*)&pois, (void*)&trace, (void*)&geo};
+                    (void*)&h, (void*)&pois, (void*)&bs_on, (void*)&trace, (void*)&geo};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(p.ctas), dim3(threads), args,
-                                         (size_t)smem, st));
+                                         (size_t)smem_res, st));
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
     if (tracing) {

@@ -26,19 +26,6 @@
 
 namespace dtb {
 
-__device__ __forceinline__ int ld_acquire_cta(const int* p) {
-  int v;
-  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];"
-               : "=r"(v)
-               : "r"((uint32_t)__cvta_generic_to_shared(p))
-               : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_cta(int* p, int v) {
-  asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(p)),
-               "r"(v)
-               : "memory");
-}
 __device__ __forceinline__ void pipe_cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
