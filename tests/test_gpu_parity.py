@@ -234,3 +234,39 @@ def test_pipe_kernel_fp32_and_large():
     assert same(out.data, jacobi_c(g.data, W02.astuple(), 24))
     out, _ = run_dtb_b200(g, W02, 16, flags=PIPE, dtype=np.float32)
     assert same(out.data.astype(np.float32), jacobi_c(g.data, W02.astuple(), 16, np.float32))
+
+
+def _device_bitwise_vs_naive(nx, ny, steps, dtype, seed=1):
+    """Full-size check without a CPU oracle: the chosen schedule and the naive
+    one-step-per-launch kernel (an independent code path) on device buffers."""
+    import torch
+    from paper_2306_03336_b200 import j2d5pt_device
+    from paper_2306_03336_b200.prng import fill_random_device
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    pitch = (nx + 2 + 31) // 32 * 32
+    a = torch.empty((ny + 2, pitch), dtype=tdt, device="cuda")
+    fill_random_device(a, nx, ny, seed, ghost=0.125)
+    b = torch.empty_like(a)
+    c = torch.empty_like(a)
+    j2d5pt_device(a, b, nx, ny, MIXED, steps)
+    j2d5pt_device(a, c, nx, ny, MIXED, steps, flags=_native.FLAG_FORCE_NAIVE)
+    torch.cuda.synchronize()
+    ib = torch.int64 if dtype == "f64" else torch.int32
+    eq = torch.equal(b[:, :nx + 2].view(ib), c[:, :nx + 2].view(ib))
+    del a, b, c
+    torch.cuda.empty_cache()
+    return eq
+
+
+def test_c4_full_size_vs_naive():
+    # BASELINE config C4 geometry (16384^2 fp64, pipe), two full 8-step passes
+    assert _device_bitwise_vs_naive(16384, 16384, 16, "f64")
+
+
+def test_c5_full_domain_single_gpu_vs_naive():
+    # BASELINE config C5's whole 32768^2 fp64 domain on one B200 (8.6 GB per buffer)
+    assert _device_bitwise_vs_naive(32768, 32768, 9, "f64", seed=5)
+
+
+def test_c3b_full_size_fp32_vs_naive():
+    assert _device_bitwise_vs_naive(8192, 8192, 20, "f32", seed=2)
