@@ -270,3 +270,28 @@ def test_c5_full_domain_single_gpu_vs_naive():
 
 def test_c3b_full_size_fp32_vs_naive():
     assert _device_bitwise_vs_naive(8192, 8192, 20, "f32", seed=2)
+
+
+def test_randomized_shapes_every_mode():
+    """Fuzz across the planner's mode boundaries (resident / pipe / tile
+    streaming / forced depths), odd sizes, both dtypes, mixed-sign weights."""
+    rng = np.random.default_rng(20261018)
+    PIPE_, RES = _native.FLAG_FORCE_PIPE, _native.FLAG_FORCE_RESIDENT
+    for case in range(28):
+        nx = int(rng.integers(1, 700))
+        ny = int(rng.integers(1, 700))
+        steps = int(rng.integers(1, 40))
+        dt = np.float32 if case % 3 == 2 else np.float64
+        g = rgrid(nx, ny, 1000 + case, ghost=float(rng.choice([0.0, 0.375, -1.5])))
+        w = StencilWeights(*(float(x) for x in rng.uniform(-0.6, 0.6, 5)))
+        want = jacobi_c(g.data, w.astuple(), steps, dt)
+        for flags, depth in ((0, None), (STREAM, None), (PIPE_, None), (RES, None),
+                             (0, int(rng.integers(1, 9)))):
+            if depth is not None and steps % depth:
+                continue
+            try:
+                out, _ = run_dtb_b200(g, w, steps, dtype=dt, flags=flags, depth=depth)
+            except Exception as e:  # a forced mode may not fit this shape
+                assert "fit" in str(e) or "feasible" in str(e) or "resident" in str(e), e
+                continue
+            assert same(out.data.astype(dt), want), (nx, ny, steps, dt, flags, depth)
