@@ -23,6 +23,7 @@
 // s, cons[s] = rows ring s's reader no longer needs.
 #pragma once
 #include "dtb_core.cuh"
+#include <type_traits>
 
 namespace dtb {
 
@@ -129,6 +130,9 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
 // steady rows: 1 stage-major pair update, 0 two row updates (fp64 faster
 // with two, fp32 with the pair: B200 A/B, round 1)
 #define DTB_PIPE_ROW2 (sizeof(T) == 4)
+#endif
+#ifndef DTB_PIPE_SPEC
+#define DTB_PIPE_SPEC 1  // role-specialised steady loops, incremental ring slots
 #endif
 #ifndef DTB_PIPE_SLEEP
 #define DTB_PIPE_SLEEP 400  // ns between ring-counter polls (fp32 +2.5 %, fp64 flat vs 20)
@@ -285,6 +289,87 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
     DTB_PIPE_ITER(t1, t2, t3, t0, b2, b1, b0, b3)
     DTB_PIPE_ITER(t2, t3, t0, t1, b3, b2, b1, b0)
     // steady: r .. r+3 all interior (r-2 >= 1, r+3+2 < Lh, r+3 < Lh-1)
+#if DTB_PIPE_SPEC
+    // role-specialised copies of the steady loop (no role branches per row)
+    // with ring slots advanced incrementally (no modulo per row)
+    auto steady = [&](auto role_c) {
+      constexpr int ROLE = decltype(role_c)::value;
+      constexpr int RIN = ROLE == 0 ? kRing0Rows : kRingRows;
+      const uint32_t in_end = ring_in + (uint32_t)RIN * RB;
+      const uint32_t out_end = ring_out + (uint32_t)kRingRows * RB;
+      uint32_t in_a = ring_in + (uint32_t)((seq0 + r + 2) % RIN) * RB;
+      uint32_t out_a = ring_out + (uint32_t)((seq0 + r - 2) % kRingRows) * RB;
+      uint32_t pf_a = ring_in + (uint32_t)((seq0 + r + 2 + kPrefetch) % RIN) * RB;
+      const T* pf_g = src + (int64_t)(pt.gy0 + r + 2 + kPrefetch) * pitch + pt.gx0;
+      T* st_g = dst + (int64_t)(pt.gy0 + r - 2) * pitch + pt.gx0 + c_lo;
+#define DTB_PIPE_SPEC_ROW(TM1, TC, TP1, TP2, BR, BM1, BM2, BM3)                   \
+  {                                                                               \
+    if constexpr (ROLE == 0) {                                                    \
+      if (r + 2 + kPrefetch < Lh) {                                               \
+        _Pragma("unroll") for (int j = 0; j < CH; ++j) {                          \
+          const int cb = (lane * CH + j) * E;                                     \
+          if (pt.vec && cb + E <= pt.Lw) {                                        \
+            pipe_cp_async16(pf_a + off[j], pf_g + cb);                            \
+          } else {                                                                \
+            _Pragma("unroll") for (int e = 0; e < E; ++e) if (cb + e < pt.Lw)     \
+                pipe_cp_async(pf_a + off[j] + (uint32_t)(e * sizeof(T)), pf_g + cb + e); \
+          }                                                                       \
+        }                                                                         \
+      }                                                                           \
+      pipe_commit();                                                              \
+      pipe_wait_group<kPrefetch>();                                               \
+      pf_a += RB;                                                                 \
+      if (pf_a == in_end) pf_a = ring_in;                                         \
+      pf_g += pitch;                                                              \
+    }                                                                             \
+    load_row_at<CH>(in_a, off, TP2);                                              \
+    in_a += RB;                                                                   \
+    if (in_a == in_end) in_a = ring_in;                                           \
+    if (DTB_PIPE_ROW2) {                                                          \
+      row_update2<T, K, DYN>(TM1, TC, TP1, BR, BM3, BM2, BM1, o, wt, lc);         \
+    } else {                                                                      \
+      row_update<T, K, DYN>(TM1, TC, TP1, BR, wt, lc);                            \
+      row_update<T, K, DYN>(BM3, BM2, BM1, o, wt, lc);                            \
+    }                                                                             \
+    if constexpr (ROLE == 2) {                                                    \
+      if (r - 2 >= pt.oy0 && r - 2 < pt.oy1) {                                    \
+        if (full_vec) {                                                           \
+          typedef typename Arith<T>::vec_t V;                                     \
+          _Pragma("unroll") for (int j = 0; j < CH; ++j) {                        \
+            V x;                                                                  \
+            T* px = reinterpret_cast<T*>(&x);                                     \
+            _Pragma("unroll") for (int e = 0; e < E; ++e) px[e] = o[j * E + e];   \
+            *reinterpret_cast<V*>(st_g + j * E) = x;                              \
+          }                                                                       \
+        } else {                                                                  \
+          _Pragma("unroll") for (int e = 0; e < K; ++e)                           \
+              if (c_lo + e >= pt.ox0 && c_lo + e < pt.ox1) st_g[e] = o[e];        \
+        }                                                                         \
+      }                                                                           \
+      st_g += pitch;                                                              \
+    } else {                                                                      \
+      store_row_at<CH>(out_a, off, o);                                            \
+      out_a += RB;                                                                \
+      if (out_a == out_end) out_a = ring_out;                                     \
+    }                                                                             \
+    ++r;                                                                          \
+  }
+      while (r + 6 < Lh) {
+        wait_in(r + 5);
+        wait_out(r + 1);
+        DTB_PIPE_SPEC_ROW(t3, t0, t1, t2, b0, b3, b2, b1)
+        DTB_PIPE_SPEC_ROW(t0, t1, t2, t3, b1, b0, b3, b2)
+        DTB_PIPE_SPEC_ROW(t1, t2, t3, t0, b2, b1, b0, b3)
+        DTB_PIPE_SPEC_ROW(t2, t3, t0, t1, b3, b2, b1, b0)
+        release_in(r);
+        release_out(r - 2);
+      }
+#undef DTB_PIPE_SPEC_ROW
+    };
+    if (first) steady(std::integral_constant<int, 0>{});
+    else if (lastst) steady(std::integral_constant<int, 2>{});
+    else steady(std::integral_constant<int, 1>{});
+#else
     while (r + 6 < Lh) {
       // one flow-control handshake per 4 rows: inputs r+2..r+5, outputs r-2..r+1
       wait_in(r + 5);
@@ -296,6 +381,7 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
       release_in(r);       // rows < r are consumed (r+0, r+1 may still be loading)
       release_out(r - 2);  // outputs < r-2 written
     }
+#endif
     // tail until every output row is out (r = Lh + 1 is the last iteration)
     while (r <= Lh + 1) {
       DTB_PIPE_ITER(t3, t0, t1, t2, b0, b3, b2, b1)
