@@ -14,7 +14,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libdtb_b200.so")
 SOURCES = ["dtb_kernels.cu", "dtb_plan.cpp"]
-HEADERS = ["dtb_core.cuh", "dtb_plan.h", os.path.join("..", "..", "include", "dtb_b200.h")]
+HEADERS = ["dtb_core.cuh", "dtb_pipe.cuh", "dtb_plan.h",
+           os.path.join("..", "..", "include", "dtb_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -28,6 +29,7 @@ def _stale() -> bool:
         return True
     t = os.path.getmtime(OUT)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [__file__]
+    deps += [os.path.join(CSRC, f) for f in os.listdir(CSRC)]  # any csrc file
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
