@@ -764,7 +764,7 @@ pipe_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int n
   constexpr int P = NW / S;
   typedef Tile<T, K> L;
   constexpr int RB = L::ROW * (int)sizeof(T);
-  constexpr int kRing0Rows = PipeCfg<NW>::kRing0Rows, kRingRows = PipeCfg<NW>::kRingRows;
+  constexpr int kRing0Rows = PipeCfg<NW, T>::kRing0Rows, kRingRows = PipeCfg<NW, T>::kRingRows;
   constexpr int kPipeBytes = (kRing0Rows + (S - 1) * kRingRows) * RB;
   extern __shared__ __align__(128) unsigned char smem_raw[];
 #ifndef DTB_PIPE_MAP
@@ -1398,7 +1398,7 @@ int launch_pipe(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int
 #endif
   constexpr int S = DTB_PIPE_STAGES, P = PW / S;
   auto kern = pipe_kernel<T, K, PW, S, DYN>;
-  const int pipe_bytes = (PipeCfg<PW>::kRing0Rows + (S - 1) * PipeCfg<PW>::kRingRows) *
+  const int pipe_bytes = (PipeCfg<PW, T>::kRing0Rows + (S - 1) * PipeCfg<PW, T>::kRingRows) *
                          Tile<T, K>::ROW * (int)sizeof(T);
   const int psmem = P * pipe_bytes + (int)sizeof(PipeSmem<S>) * P;
   int device;

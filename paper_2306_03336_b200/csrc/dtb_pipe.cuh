@@ -46,17 +46,20 @@ __device__ __forceinline__ void pipe_commit() { asm volatile("cp.async.commit_gr
 // per CTA width: 8 warps = 2 pipelines with deep rings, 16 warps = 4
 // pipelines with shallower rings (the smem budget). Block-level flow control
 // needs kRingRows >= 12 to stay deadlock-free (see pipe_stage).
+// fp64 rows need a deeper HBM prefetch than fp32 rows (same 1 KB per row, half
+// the cells, so half the compute per row to hide a row's latency behind)
 #ifndef DTB_PIPE_R0
-#define DTB_PIPE_R0 12
+#define DTB_PIPE_R0 16
 #endif
 #ifndef DTB_PIPE_PF
-#define DTB_PIPE_PF 6
+#define DTB_PIPE_PF 10
 #endif
-template <int NW>
+template <int NW, typename T = double>
 struct PipeCfg {
-  static constexpr int kRing0Rows = NW >= 16 ? DTB_PIPE_R0 : 16;  // warp 0's HBM prefetch ring
+  static constexpr bool kDeep = NW >= 16 && sizeof(T) == 8;
+  static constexpr int kRing0Rows = NW >= 16 ? (kDeep ? DTB_PIPE_R0 : 12) : 16;  // stage 0's HBM prefetch ring
   static constexpr int kRingRows = NW >= 16 ? 12 : 16;   // ring between consecutive warps
-  static constexpr int kPrefetch = NW >= 16 ? DTB_PIPE_PF : 8;     // HBM prefetch rows in flight
+  static constexpr int kPrefetch = NW >= 16 ? (kDeep ? DTB_PIPE_PF : 6) : 8;  // HBM rows in flight
 };
 
 struct PipeTile {
@@ -101,8 +104,8 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
 #endif
   const bool first = DTB_PIPE_ROLES ? ROLE == 0 : stage == 0;
   const bool lastst = DTB_PIPE_ROLES ? ROLE == 2 : stage == nstages_ - 1;
-  constexpr int kRing0Rows = PipeCfg<NW>::kRing0Rows, kRingRows = PipeCfg<NW>::kRingRows,
-                kPrefetch = PipeCfg<NW>::kPrefetch;
+  constexpr int kRing0Rows = PipeCfg<NW, T>::kRing0Rows, kRingRows = PipeCfg<NW, T>::kRingRows,
+                kPrefetch = PipeCfg<NW, T>::kPrefetch;
 
   // ---- input rows --------------------------------------------------------
   // stage 0: the warp prefetches its own lanes' chunks of row q into ring0
@@ -293,8 +296,8 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
     // role-specialised copies of the steady loop (no role branches per row)
     // with ring slots advanced incrementally (no modulo per row)
     auto steady = [&](auto role_c) {
-      constexpr int ROLE = decltype(role_c)::value;
-      constexpr int RIN = ROLE == 0 ? kRing0Rows : kRingRows;
+      constexpr int RL = decltype(role_c)::value;
+      constexpr int RIN = RL == 0 ? kRing0Rows : kRingRows;
       const uint32_t in_end = ring_in + (uint32_t)RIN * RB;
       const uint32_t out_end = ring_out + (uint32_t)kRingRows * RB;
       uint32_t in_a = ring_in + (uint32_t)((seq0 + r + 2) % RIN) * RB;
@@ -304,7 +307,7 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
       T* st_g = dst + (int64_t)(pt.gy0 + r - 2) * pitch + pt.gx0 + c_lo;
 #define DTB_PIPE_SPEC_ROW(TM1, TC, TP1, TP2, BR, BM1, BM2, BM3)                   \
   {                                                                               \
-    if constexpr (ROLE == 0) {                                                    \
+    if constexpr (RL == 0) {                                                      \
       if (r + 2 + kPrefetch < Lh) {                                               \
         _Pragma("unroll") for (int j = 0; j < CH; ++j) {                          \
           const int cb = (lane * CH + j) * E;                                     \
@@ -331,7 +334,7 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
       row_update<T, K, DYN>(TM1, TC, TP1, BR, wt, lc);                            \
       row_update<T, K, DYN>(BM3, BM2, BM1, o, wt, lc);                            \
     }                                                                             \
-    if constexpr (ROLE == 2) {                                                    \
+    if constexpr (RL == 2) {                                                      \
       if (r - 2 >= pt.oy0 && r - 2 < pt.oy1) {                                    \
         if (full_vec) {                                                           \
           typedef typename Arith<T>::vec_t V;                                     \

@@ -380,8 +380,9 @@ bool plan_pipe(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& d
   const int64_t ntiles = (int64_t)ntx * nseg;
   best.ctas = (int)std::min<int64_t>(dev.sms, (ntiles + P - 1) / P);
   best.ctas_per_sm = 1;
-  const int ring = W >= 16 ? 12 : 16;
-  best.smem_bytes = (int64_t)(ring + (S - 1) * ring) * Lw_max * elem * P;
+  // dtb_pipe.cuh PipeCfg: stage 0's prefetch ring is deeper for fp64
+  const int ring = W >= 16 ? 12 : 16, ring0 = (W >= 16 && elem == 8) ? 16 : ring;
+  best.smem_bytes = (int64_t)(ring0 + (S - 1) * ring) * Lw_max * elem * P;
   // cost: all lane-cells of every pass at ~70% of the FP issue rate + fill
   double lane_cells = 0;
   for (int i = 0; i < sx.n; ++i)
