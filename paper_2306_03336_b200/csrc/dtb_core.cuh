@@ -182,6 +182,10 @@ struct LaneCtx {
   bool first;  // lane holds frozen column 0
   bool last;   // lane holds frozen column Lw-1
   int last_e;  // its element index (== K-1 unless DYN)
+  bool fz = true;  // warp-uniform: the tile has a frozen column at all (the
+                   // resident kernel freezes only domain-ghost columns; a halo
+                   // side's outer column may go stale — its error front moves
+                   // one column per step like the frozen frame's, planner.py:272-286)
 };
 
 // Packed FP32 (sm_100a fma/add.rn.f32x2): two cells per instruction, each
@@ -190,6 +194,9 @@ struct LaneCtx {
 // instruction issues at half rate, so the element rate equals scalar FP32
 // (tools/microbench/f32x2.cu); it only frees issue slots. Measured no gain
 // for the resident sweep and spills in the 128-register pipe: off by default.
+#ifndef DTB_FZ_BRANCH
+#define DTB_FZ_BRANCH 0  // 1: skip the frozen-column selects when the tile has none (no gain measured)
+#endif
 #ifndef DTB_F32X2
 #define DTB_F32X2 0  // off: same element rate as scalar FP32 on B200 (packed ops issue at half rate)
 #endif
@@ -270,6 +277,7 @@ __device__ __forceinline__ void row_update(const T (&up)[K], const T (&mid)[K], 
       out[e] = cell_update(wv, ev, up[e], mid[e], dn[e], wt);
     }
   }
+  if (DTB_FZ_BRANCH && !lc.fz) return;
   if (lc.first) out[0] = mid[0];
   if (DYN) {
     if (lc.last) {
@@ -327,6 +335,7 @@ __device__ __forceinline__ void row_update2(const T (&ua)[K], const T (&ma)[K], 
     ob[e] = A::add(ob[e], A::mul(db[e], wt.n));
   }
   }
+  if (DTB_FZ_BRANCH && !lc.fz) return;
   if (lc.first) { oa[0] = ma[0]; ob[0] = mb[0]; }
   if (DYN) {
     if (lc.last) {
@@ -825,15 +834,17 @@ __device__ __forceinline__ void last_sweep_band(int Lh, int h, int nw, int w, in
 template <typename T, int K, bool DYN, int GT = 0>
 __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
                              const Weights<T>& wt, const Publisher<T, K>* pub = nullptr,
-                             int* bsmem = nullptr, int* bseq = nullptr) {
+                             int* bsmem = nullptr, int* bseq = nullptr,
+                             bool freeze_l = true, bool freeze_r = true) {
   const int warp = gt_tid<GT>() >> 5;
   const int nw = gt_n<GT>() >> 5;
   LaneCtx lc;
   lc.lane = threadIdx.x & 31;
   const LaneAddr<T, K> la(tile, lc.lane);
-  lc.first = (lc.lane == 0);
-  lc.last = (lc.lane == (Lw - 1) / K);
+  lc.first = freeze_l && (lc.lane == 0);
+  lc.last = freeze_r && (lc.lane == (Lw - 1) / K);
   lc.last_e = (Lw - 1) % K;
+  lc.fz = freeze_l || freeze_r;
   const int rows = Lh - 2;
   if (rows <= 0 || Lw <= 2) return;
   Publisher<T, K> nopub;

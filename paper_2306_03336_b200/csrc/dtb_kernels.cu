@@ -662,13 +662,19 @@ __device__ void poison_rim(T* tile, int Lw, int Lh, int done, bool hl, bool hr, 
   }
 }
 
+#ifndef DTB_FREEZE_HALO_COLS
+#define DTB_FREEZE_HALO_COLS 1  // 0: freeze only domain-ghost columns (parity-green, no gain)
+#endif
 template <typename T, int K, bool DYN, int GT = 0>
 __device__ void advance(T* tile, int Lw, int Lh, int steps, const Weights<T>& wt, bool poison,
                         bool hl, bool hr, bool ht, bool hb,
                         const Publisher<T, K>* pub = nullptr, int* bsmem = nullptr,
                         int* bseq = nullptr) {
   if (!poison) {
-    advance_tile<T, K, DYN, GT>(tile, Lw, Lh, steps, wt, pub, bsmem, bseq);
+    // freeze only the domain's ghost columns; stale halo columns are harmless
+    advance_tile<T, K, DYN, GT>(tile, Lw, Lh, steps, wt, pub, bsmem, bseq,
+                                !DTB_FREEZE_HALO_COLS ? !hl : true,
+                                !DTB_FREEZE_HALO_COLS ? !hr : true);
     return;
   }
   // poison mode: one step at a time, NaN the stale rim after each

@@ -54,11 +54,14 @@ __device__ __forceinline__ void pipe_commit() { asm volatile("cp.async.commit_gr
 #ifndef DTB_PIPE_PF
 #define DTB_PIPE_PF 10
 #endif
+#ifndef DTB_PIPE_RING
+#define DTB_PIPE_RING 12
+#endif
 template <int NW, typename T = double>
 struct PipeCfg {
   static constexpr bool kDeep = NW >= 16 && sizeof(T) == 8;
   static constexpr int kRing0Rows = NW >= 16 ? (kDeep ? DTB_PIPE_R0 : 12) : 16;  // stage 0's HBM prefetch ring
-  static constexpr int kRingRows = NW >= 16 ? 12 : 16;   // ring between consecutive warps
+  static constexpr int kRingRows = NW >= 16 ? (kDeep ? DTB_PIPE_RING : 12) : 16;  // ring between stages
   static constexpr int kPrefetch = NW >= 16 ? (kDeep ? DTB_PIPE_PF : 6) : 8;  // HBM rows in flight
 };
 
