@@ -280,6 +280,31 @@ __device__ __forceinline__ void warp_g2s_chunks(uint32_t sbase, const T* __restr
   }
 }
 
+// Rows [r0, r1) x cols [c0, c1) of the tile from a dense row-major array of
+// width c1 - c0 (a neighbour's packed side columns): whole 16-byte chunks when
+// the width and c0 are chunk multiples, else element copies.
+template <typename T, int K>
+__device__ __forceinline__ void warp_g2s_packed(uint32_t sbase, const T* __restrict__ src,
+                                                int r0, int r1, int c0, int c1, int lane) {
+  typedef Tile<T, K> L;
+  constexpr int E = L::EPC;
+  const int w = c1 - c0, rows = r1 - r0;
+  if (w % E == 0 && c0 % E == 0) {
+    const int cpr = w / E, n = rows * cpr;
+    for (int i = lane; i < n; i += 32) {
+      const int q = i / cpr, j = i - q * cpr, r = r0 + q, cb = c0 + j * E;
+      cp_async16(sbase + (uint32_t)((r * L::ROW + L::swz(cb / E) * E) * (int)sizeof(T)),
+                 src + (int64_t)i * E);
+    }
+  } else {
+    const int n = rows * w;
+    for (int i = lane; i < n; i += 32) {
+      const int q = i / w, r = r0 + q, c = c0 + (i - q * w);
+      cp_async(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)), src + i);
+    }
+  }
+}
+
 // Halo refresh, warp-specialised: the ring is cut into 16 tasks (N, S, the 4
 // corners, and the W and E side columns in 5 row slices each), each owned by
 // one neighbour; a warp polls that neighbour's epoch flag and streams the
@@ -291,7 +316,9 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
                                                      const int* flags, int epoch, int ntx, int nty,
                                                      int tx, int ty, int ry0, int oy0, int oy1,
                                                      int ry1, int rx0, int ox0, int ox1, int rx1,
-                                                     unsigned long long* mark = nullptr) {
+                                                     unsigned long long* mark = nullptr,
+                                                     const T* __restrict__ sides = nullptr,
+                                                     int64_t side_cap = 0) {
   typedef Tile<T, K> L;
 #ifndef DTB_SIDE_PARTS
 #define DTB_SIDE_PARTS 1
@@ -343,6 +370,13 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
       __syncwarp();
       if (mark && polled < 0) *mark = clock64();
       polled = nb;
+    }
+    if (sides && k >= 6 && kSideParts == 1) {
+      // the neighbour's packed side array facing us: its east side for our
+      // west halo, its west side for our east halo (rows [oy0, oy1))
+      const T* src = sides + ((int64_t)nb * 2 + (dx < 0 ? 1 : 0)) * side_cap;
+      warp_g2s_packed<T, K>(sbase, src, r0, r1, c0, c1, lane);
+      continue;
     }
     warp_g2s_chunks<T, K>(sbase, g, pitch, gx0, gy0, r0, r1, c0, c1, vec, lane);
   }
@@ -844,6 +878,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
                 T* __restrict__ xb1, uint64_t* __restrict__ xs0, uint64_t* __restrict__ xs1,
                 uint32_t stamp0, int* __restrict__ flags, int64_t pitch, int nx, int ny,
                 Weights<T> wt, int64_t total_steps, int h, int poison, int bs_on,
+                T* __restrict__ xsp0, T* __restrict__ xsp1, int64_t side_cap,
                 unsigned long long* __restrict__ trace, const __grid_constant__ Geometry geo) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int GT = G > 1 ? NW * 32 : 0;  // thread group = one tile
@@ -905,6 +940,11 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
   pub.full_mask = 0;
   pub.side_mask = 0;
   pub.flag = band_flags ? flags + vcta * NW : flags + vcta;
+  pub.sw = pub.se = nullptr;
+  pub.sww = bl;
+  pub.sew = br;
+  pub.own_c0 = ox0;
+  pub.own_c1 = ox1;
   pub.cl0 = ox0;
   pub.wl = bl;
   pub.cr0 = max(ox1 - br, ox0 + bl);
@@ -933,6 +973,11 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     pub.stamp = stamp0 + (uint32_t)(epoch + 1);
     pub.epoch_val = epoch + 1;
     pub.g0 = xb + (int64_t)gy0 * pitch + gx0;
+    T* xsp = ((epoch + 1) & 1) ? xsp1 : xsp0;  // packed side arrays of this epoch
+    if (xsp) {
+      pub.sw = xsp + ((int64_t)vcta * 2 + 0) * side_cap;
+      pub.se = xsp + ((int64_t)vcta * 2 + 1) * side_cap;
+    }
     pub.g = pub.g0 + (threadIdx.x & 31) * K;
     // 1. compute the epoch; its final sweep publishes the owned band from registers
     advance<T, K, DYN, GT>(tile, Lw, Lh, steps, wt, poison != 0, hl, hr, ht, hb,
@@ -1007,7 +1052,8 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
       unsigned long long t_poll = tc;
       refresh_by_direction<T, K, GT>(tile, xb, pitch, gx0, gy0, flags, epoch * flag_per_epoch,
                                  geo.ntx, geo.nty, tx, ty, ry0, oy0, oy1, ry1, rx0, ox0, ox1,
-                                 rx1, tracing ? &t_poll : nullptr);
+                                 rx1, tracing ? &t_poll : nullptr,
+                                 (DTB_SIDEPACK && DTB_PUBREG == 6) ? xsp : nullptr, side_cap);
       if (tracing) {
         const unsigned long long now_ = clock64();
         t_wait += t_poll - tc;   // warp 0: until its first neighbour flag arrived
@@ -1305,12 +1351,25 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
     void* scratch = nullptr;
     const size_t flag_bytes = 256 + (size_t)tiles * NW * sizeof(int);
     const size_t trace_bytes = (size_t)tiles * 8 * sizeof(unsigned long long);
+    // packed side-column arrays (DTB_SIDEPACK): per tile and side, the widest
+    // side halo x the tallest load region, 16-byte aligned, two parities
+    int side_w = 0;
+    for (int i = 0; i < p.sx.n; ++i) {
+      if (i > 0) side_w = std::max(side_w, p.sx.o0[i] - p.sx.l0[i]);
+      if (i + 1 < p.sx.n) side_w = std::max(side_w, p.sx.l1[i] - p.sx.o1[i]);
+    }
+    int64_t side_cap = ((int64_t)side_w * p.sy.max_load + 3) / 4 * 4;
+    const bool packed = DTB_SIDEPACK && DTB_PUBREG == 6 && !poison && side_cap > 0;
+    const size_t side_bytes = packed ? (size_t)tiles * 2 * side_cap * sizeof(T) : 0;
+    const size_t side_off = (2 * grid_bytes + flag_bytes + trace_bytes + 511) & ~(size_t)255;
     {
       std::lock_guard<std::mutex> lk(g_mu);
-      int rc = arena_get(g_scratch[device & 15], 2 * grid_bytes + flag_bytes + trace_bytes + 256,
-                         &scratch);
+      int rc = arena_get(g_scratch[device & 15], side_off + 2 * side_bytes + 256, &scratch);
       if (rc) return rc;
     }
+    T* xsp0 = packed ? reinterpret_cast<T*>(reinterpret_cast<char*>(scratch) + side_off) : nullptr;
+    T* xsp1 = packed ? reinterpret_cast<T*>(reinterpret_cast<char*>(scratch) + side_off + side_bytes)
+                     : nullptr;
     T* xb0 = reinterpret_cast<T*>(scratch);
     T* xb1 = reinterpret_cast<T*>(reinterpret_cast<char*>(scratch) + grid_bytes);
     int* flags = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + 2 * grid_bytes);
@@ -1337,7 +1396,8 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
     void* args[] = {(void*)&d_in, (void*)&d_out, (void*)&xb0, (void*)&xb1, (void*)&xs0,
                     (void*)&xs1, (void*)&stamp0, (void*)&flags,
                     (void*)&pitch, (void*)&nx, (void*)&ny, (void*)&wt, (void*)&steps,
-                    (void*)&h, (void*)&pois, (void*)&bs_on, (void*)&trace, (void*)&geo};
+                    (void*)&h, (void*)&pois, (void*)&bs_on, (void*)&xsp0, (void*)&xsp1,
+                    (void*)&side_cap, (void*)&trace, (void*)&geo};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(p.ctas), dim3(threads), args,
                                          (size_t)smem_res, st));
     g_launches += 1;
