@@ -52,9 +52,7 @@
 #endif
 #ifndef DTB_RING
 #define DTB_RING 2      // resident halo refresh: 0 generic, 1 ring copy after one wait,
-                        // 2 warp per direction: poll that neighbour, then copy its region,
-                        // 3 warp per band: per-warp flags, each warp refreshes its own
-                        // band's side columns (+ a share of the N/S rows)
+                        // 2 warp per direction: poll that neighbour, then copy its region
 #endif
 
 namespace dtb {
@@ -194,9 +192,6 @@ struct LaneCtx {
 // instruction issues at half rate, so the element rate equals scalar FP32
 // (tools/microbench/f32x2.cu); it only frees issue slots. Measured no gain
 // for the resident sweep and spills in the 128-register pipe: off by default.
-#ifndef DTB_SIDEPACK
-#define DTB_SIDEPACK 0  // 1: dense per-tile side-column arrays for the W/E halo exchange (measured -4 %)
-#endif
 #ifndef DTB_FZ_BRANCH
 #define DTB_FZ_BRANCH 0  // 1: skip the frozen-column selects when the tile has none (no gain measured)
 #endif
@@ -414,48 +409,6 @@ __device__ __forceinline__ void gt_sync() {
     __syncthreads();
 }
 
-#ifndef DTB_XCHG
-#define DTB_XCHG 0  // resident exchange: 0 mirror grid + release/acquire epoch flags,
-                    // 1 stamped words (every 8-byte word carries the epoch stamp in its
-                    // high half: no fence, no flag; readers check each word)
-#endif
-
-// Stamped exchange words: value bits in the low 32 bits, the epoch stamp in the
-// high 32; fp64 values take two words (lo, hi). Each 8-byte word is one
-// single-copy-atomic access, so a reader that sees the stamp sees the payload.
-template <typename T>
-struct Stamped {
-  static constexpr int WPV = sizeof(T) == 8 ? 2 : 1;  // words per value
-};
-__device__ __forceinline__ void st_stamped(uint64_t* p, double v, uint32_t stamp) {
-  const uint64_t b = (uint64_t)__double_as_longlong(v), hi = (uint64_t)stamp << 32;
-  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p),
-               "l"(hi | (b & 0xffffffffull)), "l"(hi | (b >> 32)) : "memory");
-}
-__device__ __forceinline__ void st_stamped(uint64_t* p, float v, uint32_t stamp) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p),
-               "l"(((uint64_t)stamp << 32) | __float_as_uint(v)) : "memory");
-}
-struct StampedLoad {  // one value's words in flight
-  uint64_t a, b;
-};
-__device__ __forceinline__ void ld_stamped(const uint64_t* p, StampedLoad& w, double) {
-  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w.a), "=l"(w.b) : "l"(p) : "memory");
-}
-__device__ __forceinline__ void ld_stamped(const uint64_t* p, StampedLoad& w, float) {
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w.a) : "l"(p) : "memory");
-  w.b = w.a;
-}
-__device__ __forceinline__ bool stamped_ok(const StampedLoad& w, uint32_t stamp) {
-  return (uint32_t)(w.a >> 32) == stamp && (uint32_t)(w.b >> 32) == stamp;
-}
-__device__ __forceinline__ double stamped_value(const StampedLoad& w, double) {
-  return __longlong_as_double((long long)((w.a & 0xffffffffull) | (w.b << 32)));
-}
-__device__ __forceinline__ float stamped_value(const StampedLoad& w, float) {
-  return __uint_as_float((uint32_t)w.a);
-}
-
 // Publisher: during the last sweep of a resident epoch, every freshly
 // computed row that lies in the CTA's owned band (the cells its neighbours'
 // halos cover) is also stored straight from registers to the L2 exchange
@@ -483,17 +436,13 @@ struct Publisher {
   int64_t pitch;
   int own0, own1, top1, bot0;
   uint32_t full_mask, side_mask;
-  int* flag;        // mode 3: this CTA's epoch flag (per-warp release-add);
-                    // DTB_RING 3: this CTA's per-warp flags (flag[warp] = epoch)
-  int epoch_val;    // DTB_RING 3: the epoch this sweep completes
+  int* flag;        // modes 3/6: this CTA's epoch flag (per-warp release-add)
   // mode 2/3: publish the band's own rows [ya, yb) from smem (they are final once
   // the band's last sweep is done: no other warp writes them)
   // mode 6: side columns flattened across lanes (lane i -> element i of the
   // band's (row, side column) list), so one warp store covers 32 / (wl + wr)
   // rows instead of one
   T* g0;            // exchange buffer at (tile row 0, tile column 0)
-  uint64_t* x;      // DTB_XCHG 1: stamped-word buffer at (tile row 0, tile column 0)
-  uint32_t stamp;   // DTB_XCHG 1: this epoch's stamp
   int cl0, wl, cr0, wr;  // side columns [cl0, cl0 + wl) and [cr0, cr0 + wr)
   __device__ __forceinline__ void put_sides(const LaneAddr<T, K>& la, int r0, int r1) const {
     typedef Tile<T, K> L;
@@ -513,56 +462,10 @@ struct Publisher {
         asm volatile("ld.shared.f32 %0, [%1];" : "=f"(f) : "r"(la.base + (uint32_t)(L::at(r, c) * 4)));
         v = (T)f;
       }
-      if (DTB_XCHG == 1) st_stamped(x + ((int64_t)r * pitch + c) * Stamped<T>::WPV, v, stamp);
-      else st_pred(true, g0 + (int64_t)r * pitch + c, v);
-    }
-  }
-  // DTB_SIDEPACK: the side columns of every owned row also go to two dense
-  // per-tile arrays (row-major, width = the neighbour's halo depth), so the
-  // stores here and the neighbour's halo loads are contiguous
-  T* sw;            // this tile's west-side array: owned cols [own_c0, own_c0 + sww)
-  T* se;            // east-side array: owned cols [own_c1 - sew, own_c1)
-  int sww, sew, own_c0, own_c1;
-  __device__ __forceinline__ void put_sides_packed(const LaneAddr<T, K>& la, int r0, int r1) const {
-    typedef Tile<T, K> L;
-    const int nwst = (r1 - r0) * sww, n = nwst + (r1 - r0) * sew;
-    const int lane = threadIdx.x & 31;
-#pragma unroll 2
-    for (int i = lane; i < n; i += 32) {
-      int r, c;
-      T* dst;
-      if (i < nwst) {
-        const int q = i / sww;
-        r = r0 + q;
-        c = own_c0 + (i - q * sww);
-        dst = sw + (int64_t)(r - own0) * sww + (i - q * sww);
-      } else {
-        const int k = i - nwst, q = k / sew;
-        r = r0 + q;
-        c = own_c1 - sew + (k - q * sew);
-        dst = se + (int64_t)(r - own0) * sew + (k - q * sew);
-      }
-      T v;
-      if (sizeof(T) == 8) {
-        double d;
-        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(d) : "r"(la.base + (uint32_t)(L::at(r, c) * 8)));
-        v = (T)d;
-      } else {
-        float f;
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(f) : "r"(la.base + (uint32_t)(L::at(r, c) * 4)));
-        v = (T)f;
-      }
-      st_pred(true, dst, v);
+      st_pred(true, g0 + (int64_t)r * pitch + c, v);
     }
   }
   __device__ __forceinline__ void put_band(const LaneAddr<T, K>& la, int ya, int yb) const {
-    if (DTB_PUBREG == 6 && DTB_SIDEPACK) {
-      const int r0 = max(ya, own0), r1 = min(yb, own1);
-      if (r0 < r1) put_sides_packed(la, r0, r1);
-      put_rows(la, r0, min(r1, top1));
-      put_rows(la, max(r0, bot0), r1);
-      return;
-    }
     if (DTB_PUBREG == 6) {
       const int r0 = max(ya, own0), r1 = min(yb, own1);
       const int s0 = max(r0, top1), s1 = min(r1, bot0);
@@ -585,13 +488,6 @@ struct Publisher {
       for (int u = 0; u < 4; ++u) {
         const int rr = row + u;
         const uint32_t m = (rr < top1 || rr >= bot0) ? full_mask : side_mask;
-        if (DTB_XCHG == 1) {
-          uint64_t* q = x + ((int64_t)rr * pitch + (threadIdx.x & 31) * K) * Stamped<T>::WPV;
-#pragma unroll
-          for (int e = 0; e < K; ++e)
-            if ((m >> e) & 1u) st_stamped(q + e * Stamped<T>::WPV, v[u][e], stamp);
-          continue;
-        }
         T* p = g + (int64_t)rr * pitch;
 #pragma unroll
         for (int e = 0; e < K; ++e) st_pred(((m >> e) & 1u) != 0, p + e, v[u][e]);
@@ -601,13 +497,6 @@ struct Publisher {
       T v[K];
       load_row<T, K>(la, row, v);
       const uint32_t m = (row < top1 || row >= bot0) ? full_mask : side_mask;
-      if (DTB_XCHG == 1) {
-        uint64_t* q = x + ((int64_t)row * pitch + (threadIdx.x & 31) * K) * Stamped<T>::WPV;
-#pragma unroll
-        for (int e = 0; e < K; ++e)
-          if ((m >> e) & 1u) st_stamped(q + e * Stamped<T>::WPV, v[e], stamp);
-        continue;
-      }
       T* p = g + (int64_t)row * pitch;
 #pragma unroll
       for (int e = 0; e < K; ++e) st_pred(((m >> e) & 1u) != 0, p + e, v[e]);
@@ -862,21 +751,6 @@ __device__ __forceinline__ void band_rows4(int Lh, int nb, int b, int& ya, int& 
   if (b == nb - 1) yb = Lh - 1;
 }
 
-// Band [ya, yb) of warp w in the LAST sweep of an h-step epoch (two-step
-// sweeps when h is even, else a closing one-step sweep), as advance_tile lays
-// it out; ya == yb for warps without a band.
-__device__ __forceinline__ void last_sweep_band(int Lh, int h, int nw, int w, int& ya, int& yb) {
-  const int rows = Lh - 2;
-  ya = yb = 0;
-  if (h >= 2 && rows >= 2 && (h & 1) == 0) {
-    const int nb2 = max(1, min(nw, rows / 2));
-    if (w < nb2) band_rows4(Lh, nb2, w, ya, yb);
-  } else {
-    const int nb1 = max(1, min(nw, rows));
-    if (w < nb1) band_rows(Lh, nb1, w, ya, yb);
-  }
-}
-
 // Advance the tile `steps` time steps in place. All threads of the CTA call.
 // With `pub` non-null the final sweep also publishes the owned band.
 template <typename T, int K, bool DYN, int GT = 0>
@@ -922,18 +796,12 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
           // stores only; one CTA-level release after the closing barrier
         } else if (DTB_PUBREG == 2) {
           __threadfence();
-        } else if (DTB_XCHG == 1) {
-          // stamped words need no fence or flag
         } else {
           // each warp releases its own stores and bumps the CTA's epoch flag;
           // neighbours wait for nwarps bumps per epoch (no CTA barrier first)
           __syncwarp();
           if (lc.lane == 0)
-            if (DTB_RING == 3)
-              asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(pub->flag + warp),
-                           "r"(pub->epoch_val) : "memory");
-            else
-              asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
         }
       }
       if (!use_bs || s + 4 > steps) gt_sync<GT>();
@@ -952,15 +820,10 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
         if (DTB_PUBREG == 5) {
         } else if (DTB_PUBREG == 2) {
           __threadfence();
-        } else if (DTB_XCHG == 1) {
         } else {
           __syncwarp();
           if (lc.lane == 0)
-            if (DTB_RING == 3)
-              asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(pub->flag + warp),
-                           "r"(pub->epoch_val) : "memory");
-            else
-              asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
         }
       }
       gt_sync<GT>();

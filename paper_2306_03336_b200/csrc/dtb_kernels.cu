@@ -280,31 +280,6 @@ __device__ __forceinline__ void warp_g2s_chunks(uint32_t sbase, const T* __restr
   }
 }
 
-// Rows [r0, r1) x cols [c0, c1) of the tile from a dense row-major array of
-// width c1 - c0 (a neighbour's packed side columns): whole 16-byte chunks when
-// the width and c0 are chunk multiples, else element copies.
-template <typename T, int K>
-__device__ __forceinline__ void warp_g2s_packed(uint32_t sbase, const T* __restrict__ src,
-                                                int r0, int r1, int c0, int c1, int lane) {
-  typedef Tile<T, K> L;
-  constexpr int E = L::EPC;
-  const int w = c1 - c0, rows = r1 - r0;
-  if (w % E == 0 && c0 % E == 0) {
-    const int cpr = w / E, n = rows * cpr;
-    for (int i = lane; i < n; i += 32) {
-      const int q = i / cpr, j = i - q * cpr, r = r0 + q, cb = c0 + j * E;
-      cp_async16(sbase + (uint32_t)((r * L::ROW + L::swz(cb / E) * E) * (int)sizeof(T)),
-                 src + (int64_t)i * E);
-    }
-  } else {
-    const int n = rows * w;
-    for (int i = lane; i < n; i += 32) {
-      const int q = i / w, r = r0 + q, c = c0 + (i - q * w);
-      cp_async(sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T)), src + i);
-    }
-  }
-}
-
 // Halo refresh, warp-specialised: the ring is cut into 16 tasks (N, S, the 4
 // corners, and the W and E side columns in 5 row slices each), each owned by
 // one neighbour; a warp polls that neighbour's epoch flag and streams the
@@ -316,9 +291,7 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
                                                      const int* flags, int epoch, int ntx, int nty,
                                                      int tx, int ty, int ry0, int oy0, int oy1,
                                                      int ry1, int rx0, int ox0, int ox1, int rx1,
-                                                     unsigned long long* mark = nullptr,
-                                                     const T* __restrict__ sides = nullptr,
-                                                     int64_t side_cap = 0) {
+                                                     unsigned long long* mark = nullptr) {
   typedef Tile<T, K> L;
 #ifndef DTB_SIDE_PARTS
 #define DTB_SIDE_PARTS 1
@@ -371,254 +344,7 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
       if (mark && polled < 0) *mark = clock64();
       polled = nb;
     }
-    if (sides && k >= 6 && kSideParts == 1) {
-      // the neighbour's packed side array facing us: its east side for our
-      // west halo, its west side for our east halo (rows [oy0, oy1))
-      const T* src = sides + ((int64_t)nb * 2 + (dx < 0 ? 1 : 0)) * side_cap;
-      warp_g2s_packed<T, K>(sbase, src, r0, r1, c0, c1, lane);
-      continue;
-    }
     warp_g2s_chunks<T, K>(sbase, g, pitch, gx0, gy0, r0, r1, c0, c1, vec, lane);
-  }
-  cp_async_wait_all();
-}
-
-// Stamped-word refresh of the halo rectangle [r0, r1) x [c0, c1) (tile
-// coordinates) by one warp: kBatch words in flight per lane, each value
-// re-polled until its words carry this epoch's stamp, then stored to smem.
-template <typename T, int K>
-__device__ __forceinline__ void warp_refresh_stamped(uint32_t sbase, const uint64_t* __restrict__ x,
-                                                     int64_t pitch, int gx0, int gy0, int r0,
-                                                     int r1, int c0, int c1, uint32_t stamp,
-                                                     int lane) {
-  typedef Tile<T, K> L;
-  constexpr int kBatch = 8, WPV = Stamped<T>::WPV;
-  const int w = c1 - c0, n = (r1 - r0) * w;
-  for (int base = lane; base < n; base += 32 * kBatch) {
-    StampedLoad v[kBatch];
-    const uint64_t* src[kBatch];
-    uint32_t dst[kBatch];
-#pragma unroll
-    for (int j = 0; j < kBatch; ++j) {
-      const int i = base + 32 * j;
-      const int q = i / w, r = r0 + q, c = c0 + (i - q * w);
-      src[j] = x + ((int64_t)(gy0 + r) * pitch + gx0 + c) * WPV;
-      dst[j] = sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T));
-      if (i < n) ld_stamped(src[j], v[j], T());
-    }
-#pragma unroll
-    for (int j = 0; j < kBatch; ++j) {
-      if (base + 32 * j < n) {
-        while (!stamped_ok(v[j], stamp)) {
-          __nanosleep(16);
-          ld_stamped(src[j], v[j], T());
-        }
-        sts_elem(dst[j], stamped_value(v[j], T()));
-      }
-    }
-  }
-}
-
-// Halo refresh over stamped words: the (up to 8) ring rectangles are
-// flattened into one index space spread over every thread of the CTA, each
-// thread keeping all its loads in flight at once (one L2 round trip for the
-// whole ring when the neighbours have published); no flags (each word proves
-// its own epoch).
-#ifndef DTB_STAMP_BATCH
-#define DTB_STAMP_BATCH 8
-#endif
-#ifndef DTB_STAMP_SENTINEL
-#define DTB_STAMP_SENTINEL 1
-#endif
-template <typename T, int K, int GT = 0>
-__device__ __forceinline__ void refresh_stamped(T* tile, const uint64_t* __restrict__ x,
-                                                int64_t pitch, int gx0, int gy0, uint32_t stamp,
-                                                int ntx, int nty, int tx, int ty, int ry0,
-                                                int oy0, int oy1, int ry1, int rx0, int ox0,
-                                                int ox1, int rx1, unsigned long long* mark) {
-  typedef Tile<T, K> L;
-  constexpr int WPV = Stamped<T>::WPV, kBatch = DTB_STAMP_BATCH;
-  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
-  // rectangles: N, S, NW, NE, SW, SE, W, E (empty when the neighbour is absent)
-  int rr0[8], cc0[8], ww[8], end[8];
-  int total = 0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    int dx, dy, r0, r1, c0, c1;
-    switch (k) {
-      case 0: dx = 0; dy = -1; r0 = ry0; r1 = oy0; c0 = ox0; c1 = ox1; break;
-      case 1: dx = 0; dy = 1; r0 = oy1; r1 = ry1; c0 = ox0; c1 = ox1; break;
-      case 2: dx = -1; dy = -1; r0 = ry0; r1 = oy0; c0 = rx0; c1 = ox0; break;
-      case 3: dx = 1; dy = -1; r0 = ry0; r1 = oy0; c0 = ox1; c1 = rx1; break;
-      case 4: dx = -1; dy = 1; r0 = oy1; r1 = ry1; c0 = rx0; c1 = ox0; break;
-      case 5: dx = 1; dy = 1; r0 = oy1; r1 = ry1; c0 = ox1; c1 = rx1; break;
-      case 6: dx = -1; dy = 0; r0 = oy0; r1 = oy1; c0 = rx0; c1 = ox0; break;
-      default: dx = 1; dy = 0; r0 = oy0; r1 = oy1; c0 = ox1; c1 = rx1; break;
-    }
-    const int nxt = tx + dx, nyt = ty + dy;
-    const bool on = r1 > r0 && c1 > c0 && nxt >= 0 && nxt < ntx && nyt >= 0 && nyt < nty;
-    rr0[k] = r0;
-    cc0[k] = c0;
-    ww[k] = on ? c1 - c0 : 1;
-    total += on ? (r1 - r0) * (c1 - c0) : 0;
-    end[k] = total;
-#if DTB_STAMP_SENTINEL
-    // thread k first waits on one word of rectangle k (cheap polling); the
-    // bulk loads below then mostly find their stamps on the first try
-    if (on && gt_tid<GT>() == 32 * k) {
-      StampedLoad w;
-      const uint64_t* q = x + ((int64_t)(gy0 + r1 - 1) * pitch + gx0 + c1 - 1) * WPV;
-      ld_stamped(q, w, T());
-      while (!stamped_ok(w, stamp)) {
-        __nanosleep(64);
-        ld_stamped(q, w, T());
-      }
-    }
-#endif
-  }
-#if DTB_STAMP_SENTINEL
-  gt_sync<GT>();
-#endif
-  if (mark) *mark = clock64();
-  for (int base = gt_tid<GT>(); base < total; base += gt_n<GT>() * kBatch) {
-    StampedLoad v[kBatch];
-    const uint64_t* src[kBatch];
-    uint32_t dst[kBatch];
-#pragma unroll
-    for (int j = 0; j < kBatch; ++j) {
-      const int i = base + gt_n<GT>() * j;
-      int k = 0, st0 = 0;
-#pragma unroll
-      for (int q = 0; q < 7; ++q)
-        if (i >= end[q]) { k = q + 1; st0 = end[q]; }
-      int r0 = rr0[0], c0 = cc0[0], w = ww[0];
-#pragma unroll
-      for (int q = 1; q < 8; ++q)
-        if (k == q) { r0 = rr0[q]; c0 = cc0[q]; w = ww[q]; }
-      const int li = i - st0, qr = li / w, r = r0 + qr, c = c0 + (li - qr * w);
-      src[j] = x + ((int64_t)(gy0 + r) * pitch + gx0 + c) * WPV;
-      dst[j] = sbase + (uint32_t)(L::at(r, c) * (int)sizeof(T));
-      if (i < total) ld_stamped(src[j], v[j], T());
-    }
-    // retire the words that carry the stamp; re-poll the rest together (one
-    // round trip per retry, not one per late word)
-    uint32_t pending = 0;
-#pragma unroll
-    for (int j = 0; j < kBatch; ++j)
-      if (base + gt_n<GT>() * j < total) pending |= 1u << j;
-    while (true) {
-#pragma unroll
-      for (int j = 0; j < kBatch; ++j) {
-        if (((pending >> j) & 1u) && stamped_ok(v[j], stamp)) {
-          sts_elem(dst[j], stamped_value(v[j], T()));
-          pending &= ~(1u << j);
-        }
-      }
-      if (!pending) break;
-      __nanosleep(32);
-#pragma unroll
-      for (int j = 0; j < kBatch; ++j)
-        if ((pending >> j) & 1u) ld_stamped(src[j], v[j], T());
-    }
-  }
-}
-
-// DTB_RING 3: wait until every warp of neighbour tile `nb` whose last-sweep
-// band intersects its rows [r0, r1) has published epoch `epoch` (lanes poll
-// one producer warp each).
-__device__ __forceinline__ void wait_band_flags(const int* flags, int nb, int nw, int Lh_p, int h,
-                                                int r0, int r1, int epoch, int lane) {
-  if (lane < nw) {
-    int ya, yb;
-    last_sweep_band(Lh_p, h, nw, lane, ya, yb);
-    if (ya < yb && ya < r1 && yb > r0) {
-      const int* f = flags + nb * nw + lane;
-      // relaxed polls (no L1 invalidate per poll while other warps' cp.async
-      // are in flight), one acquire once the flag is seen
-      while (ld_relaxed_gpu(f) < epoch) __nanosleep(32);
-      (void)ld_acquire_gpu(f);
-    }
-  }
-  __syncwarp();
-}
-
-// DTB_RING 3 halo refresh: warp w copies the W/E side columns of its own band's
-// owned rows (from the W/E neighbours' same-numbered bands) and, split by rows
-// across the first / second half of the warps, the N / S halo rows including
-// the corners. Only the producing warps' flags are awaited.
-template <typename T, int K, int GT = 0>
-__device__ __forceinline__ void refresh_by_band(T* tile, const T* __restrict__ g, int64_t pitch,
-                                                int gx0, int gy0, const int* flags, int epoch,
-                                                const Geometry& geo, int tx, int ty, int Lh, int h,
-                                                int ry0, int oy0, int oy1, int ry1, int rx0,
-                                                int ox0, int ox1, int rx1,
-                                                unsigned long long* mark) {
-  typedef Tile<T, K> L;
-  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
-  const int warp = gt_tid<GT>() >> 5, lane = threadIdx.x & 31, nw = gt_n<GT>() >> 5;
-  const bool vec = ((gx0 % L::EPC) == 0) && ((pitch % L::EPC) == 0);
-  const int ntx = geo.ntx, nty = geo.nty;
-  // (a) side columns of this warp's band rows
-  int ya, yb;
-  last_sweep_band(Lh, h, nw, warp, ya, yb);
-  const int r0 = max(ya, oy0), r1 = min(yb, oy1);
-  const bool west = r0 < r1 && tx > 0 && rx0 < ox0;
-  const bool east = r0 < r1 && tx + 1 < ntx && ox1 < rx1;
-  // (b) N rows [ry0, oy0) on warps [0, G), S rows [oy1, ry1) on warps [G, nw)
-  const int G = max(1, nw / 2);
-  const bool north = warp < G;
-  const int nyt = ty + (north ? -1 : 1);
-  const int j = north ? warp : warp - G, nj = north ? G : nw - G;
-  const int q0 = north ? ry0 : oy1, q1 = north ? oy0 : ry1;
-  const bool rows_task = nyt >= 0 && nyt < nty && q0 < q1 && j < nj && q0 + j < q1;
-  int Lh_p = 0, shift = 0;
-  if (rows_task) {
-    const int4 cyn = geo.row[nyt];
-    Lh_p = cyn.w - cyn.z;
-    shift = (geo.row[ty].z + 1) - (cyn.z + 1);  // my tile row -> theirs
-  }
-  // every wait first, all in parallel: lane c polls candidate c (neighbour k
-  // of W, E, NW, N, NE / SW, S, SE x producer warp w) when that warp's
-  // last-sweep band covers rows this warp copies from that neighbour
-#pragma unroll
-  for (int rep = 0; rep < 2; ++rep) {
-    const int c = lane + 32 * rep, k = c / nw, w = c % nw;
-    if (k < 5) {
-      int nbx = tx, nby = ty, lo = 0, hi = 0, lhp = Lh;
-      bool need = false;
-      if (k == 0 && west) { nbx = tx - 1; lo = r0; hi = r1; need = true; }
-      if (k == 1 && east) { nbx = tx + 1; lo = r0; hi = r1; need = true; }
-      if (k >= 2 && rows_task) {
-        const int dx = k - 3;
-        const int c0 = dx < 0 ? rx0 : (dx == 0 ? ox0 : ox1);
-        const int c1 = dx < 0 ? ox0 : (dx == 0 ? ox1 : rx1);
-        nbx = tx + dx;
-        nby = nyt;
-        lo = q0 + j + shift;
-        hi = q1 + shift;
-        lhp = Lh_p;
-        need = nbx >= 0 && nbx < ntx && c0 < c1;
-      }
-      if (need) {
-        int ya2, yb2;
-        last_sweep_band(lhp, h, nw, w, ya2, yb2);
-        if (ya2 < yb2 && ya2 < hi && yb2 > lo) {
-          const int* f = flags + (nby * ntx + nbx) * nw + w;
-          while (ld_relaxed_gpu(f) < epoch) __nanosleep(32);
-          (void)ld_acquire_gpu(f);
-        }
-      }
-    }
-  }
-  __syncwarp();
-  if (mark) *mark = clock64();
-  if (west) warp_g2s_chunks<T, K>(sbase, g, pitch, gx0, gy0, r0, r1, rx0, ox0, vec, lane);
-  if (east) warp_g2s_chunks<T, K>(sbase, g, pitch, gx0, gy0, r0, r1, ox1, rx1, vec, lane);
-  if (rows_task) {
-    for (int r = q0 + j; r < q1; r += nj) {
-      const int c0 = tx > 0 ? rx0 : ox0, c1 = tx + 1 < ntx ? rx1 : ox1;
-      warp_g2s_chunks<T, K>(sbase, g, pitch, gx0, gy0, r, r + 1, c0, c1, vec, lane);
-    }
   }
   cp_async_wait_all();
 }
@@ -875,10 +601,8 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
 template <typename T, int K, int NW, bool DYN, int G = 1>
 __global__ void __launch_bounds__(NW * 32 * G, 1)
 resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ xb0,
-                T* __restrict__ xb1, uint64_t* __restrict__ xs0, uint64_t* __restrict__ xs1,
-                uint32_t stamp0, int* __restrict__ flags, int64_t pitch, int nx, int ny,
+                T* __restrict__ xb1, int* __restrict__ flags, int64_t pitch, int nx, int ny,
                 Weights<T> wt, int64_t total_steps, int h, int poison, int bs_on,
-                T* __restrict__ xsp0, T* __restrict__ xsp1, int64_t side_cap,
                 unsigned long long* __restrict__ trace, const __grid_constant__ Geometry geo) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int GT = G > 1 ? NW * 32 : 0;  // thread group = one tile
@@ -930,7 +654,6 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     tc = now_;                                         \
   }
   // per-lane publish masks over the lane's K columns (tile coordinates)
-  const bool band_flags = DTB_RING == 3 && !poison && (DTB_PUBREG == 3 || DTB_PUBREG == 6);
   Publisher<T, K> pub;
   pub.pitch = pitch;
   pub.own0 = oy0;
@@ -939,21 +662,15 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
   pub.bot0 = oy1 - bb;
   pub.full_mask = 0;
   pub.side_mask = 0;
-  pub.flag = band_flags ? flags + vcta * NW : flags + vcta;
-  pub.sw = pub.se = nullptr;
-  pub.sww = bl;
-  pub.sew = br;
-  pub.own_c0 = ox0;
-  pub.own_c1 = ox1;
+  pub.flag = flags + vcta;
   pub.cl0 = ox0;
   pub.wl = bl;
   pub.cr0 = max(ox1 - br, ox0 + bl);
   pub.wr = ox1 - pub.cr0;
   // flag value that marks "epoch e published": e (CTA-level release) or
   // e * warps (mode 3: one release-add per warp)
-  const bool stamped = DTB_XCHG == 1 && !poison;
-  const int flag_per_epoch = band_flags ? 0 :
-      (((DTB_PUBREG == 3 || DTB_PUBREG == 4 || DTB_PUBREG == 6) && !poison) ? NW : 1);
+  const int flag_per_epoch =
+      ((DTB_PUBREG == 3 || DTB_PUBREG == 4 || DTB_PUBREG == 6) && !poison) ? NW : 1;
   {
     const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -969,15 +686,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     const int steps = (int)((total_steps - done) < (int64_t)h ? (total_steps - done) : (int64_t)h);
     const bool last = done + steps >= total_steps;
     T* xb = ((epoch + 1) & 1) ? xb1 : xb0;
-    pub.x = (((epoch + 1) & 1) ? xs1 : xs0) + ((int64_t)gy0 * pitch + gx0) * Stamped<T>::WPV;
-    pub.stamp = stamp0 + (uint32_t)(epoch + 1);
-    pub.epoch_val = epoch + 1;
     pub.g0 = xb + (int64_t)gy0 * pitch + gx0;
-    T* xsp = ((epoch + 1) & 1) ? xsp1 : xsp0;  // packed side arrays of this epoch
-    if (xsp) {
-      pub.sw = xsp + ((int64_t)vcta * 2 + 0) * side_cap;
-      pub.se = xsp + ((int64_t)vcta * 2 + 1) * side_cap;
-    }
     pub.g = pub.g0 + (threadIdx.x & 31) * K;
     // 1. compute the epoch; its final sweep publishes the owned band from registers
     advance<T, K, DYN, GT>(tile, Lw, Lh, steps, wt, poison != 0, hl, hr, ht, hb,
@@ -986,19 +695,6 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     DTB_MARK(t_comp)
     if (last) break;
     ++epoch;
-    if (stamped) {
-      unsigned long long t_s = 0;
-      // 2+3. stamped words: no barrier, fence or flag; each warp polls its
-      // ring tasks' words and stores them as they arrive
-      refresh_stamped<T, K, GT>(tile, (epoch & 1) ? xs1 : xs0, pitch, gx0, gy0,
-                            stamp0 + (uint32_t)epoch, geo.ntx, geo.nty, tx, ty, ry0, oy0, oy1,
-                            ry1, rx0, ox0, ox1, rx1, tracing ? &t_s : nullptr);
-      if (tracing) t_pst += t_s - tc;
-      DTB_MARK(t_wait)
-      gt_sync<GT>();
-      DTB_MARK(t_ref)
-      continue;
-    }
     if (!poison && DTB_PUBREG == 0) {
       const int t1 = min(oy0 + bt, oy1), b0 = max(oy1 - bb, t1);
       publish_band<T, K, GT>(tile, xb, pitch, gx0, gy0, oy0, t1, b0, oy1, ox0, ox0 + bl,
@@ -1026,18 +722,6 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     DTB_MARK(t_pst)
     if (DTB_FENCE == 1) __threadfence();
     // per-warp release modes need no CTA barrier here: advance() closed with one
-    if (band_flags) {
-      // 2+3. per band: no CTA barrier before (advance() closed with one)
-      DTB_MARK(t_pbar)
-      unsigned long long t_w = tc;
-      refresh_by_band<T, K, GT>(tile, xb, pitch, gx0, gy0, flags, epoch, geo, tx, ty, Lh, h, ry0,
-                            oy0, oy1, ry1, rx0, ox0, ox1, rx1, tracing ? &t_w : nullptr);
-      if (tracing) t_pub += t_w - tc;  // warp 0: flag waits
-      DTB_MARK(t_wait)
-      gt_sync<GT>();
-      DTB_MARK(t_ref)
-      continue;
-    }
     if (flag_per_epoch == 1 || DTB_SKIPBAR == 0) gt_sync<GT>();
     DTB_MARK(t_pbar)
     if (gt_tid<GT>() == 0 && flag_per_epoch == 1) {
@@ -1052,8 +736,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
       unsigned long long t_poll = tc;
       refresh_by_direction<T, K, GT>(tile, xb, pitch, gx0, gy0, flags, epoch * flag_per_epoch,
                                  geo.ntx, geo.nty, tx, ty, ry0, oy0, oy1, ry1, rx0, ox0, ox1,
-                                 rx1, tracing ? &t_poll : nullptr,
-                                 (DTB_SIDEPACK && DTB_PUBREG == 6) ? xsp : nullptr, side_cap);
+                                 rx1, tracing ? &t_poll : nullptr);
       if (tracing) {
         const unsigned long long now_ = clock64();
         t_wait += t_poll - tc;   // warp 0: until its first neighbour flag arrived
@@ -1196,38 +879,6 @@ int arena_get(Arena& a, size_t bytes, void** out) {
   return DTB_OK;
 }
 
-// Stamped-word exchange buffers (DTB_XCHG 1): dedicated per device, zeroed on
-// allocation; every resident epoch ever run on them gets a fresh stamp, so a
-// word left by an earlier epoch or launch can never pass a reader's check.
-struct StampArena {
-  void* p = nullptr;
-  size_t n = 0;
-  uint32_t next = 1;
-};
-StampArena g_stamped[16];
-
-int stamped_get(StampArena& a, size_t bytes, int64_t epochs, cudaStream_t st, uint64_t** out,
-                uint32_t* stamp0) {
-  if (a.n < bytes) {
-    if (a.p) cudaFree(a.p);
-    a.p = nullptr;
-    a.n = 0;
-    CUDA_TRY(cudaMalloc(&a.p, bytes));
-    a.n = bytes;
-    CUDA_TRY(cudaMemsetAsync(a.p, 0, bytes, st));
-    a.next = 1;
-  }
-  if ((int64_t)a.next + epochs + 2 > 0x7fffffffLL) {
-    if (epochs + 3 > 0x7fffffffLL) return fail(DTB_ERANGE, "too many resident epochs (%lld)", (long long)epochs);
-    CUDA_TRY(cudaMemsetAsync(a.p, 0, a.n, st));
-    a.next = 1;
-  }
-  *stamp0 = a.next;
-  a.next += (uint32_t)(epochs + 1);
-  *out = reinterpret_cast<uint64_t*>(a.p);
-  return DTB_OK;
-}
-
 // Per-call host work is on the critical path of short solves (C1: ~0.1 ms per
 // solve), so device attributes, kernel smem attributes and occupancy are
 // queried once per device / kernel and cached.
@@ -1351,25 +1002,12 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
     void* scratch = nullptr;
     const size_t flag_bytes = 256 + (size_t)tiles * NW * sizeof(int);
     const size_t trace_bytes = (size_t)tiles * 8 * sizeof(unsigned long long);
-    // packed side-column arrays (DTB_SIDEPACK): per tile and side, the widest
-    // side halo x the tallest load region, 16-byte aligned, two parities
-    int side_w = 0;
-    for (int i = 0; i < p.sx.n; ++i) {
-      if (i > 0) side_w = std::max(side_w, p.sx.o0[i] - p.sx.l0[i]);
-      if (i + 1 < p.sx.n) side_w = std::max(side_w, p.sx.l1[i] - p.sx.o1[i]);
-    }
-    int64_t side_cap = ((int64_t)side_w * p.sy.max_load + 3) / 4 * 4;
-    const bool packed = DTB_SIDEPACK && DTB_PUBREG == 6 && !poison && side_cap > 0;
-    const size_t side_bytes = packed ? (size_t)tiles * 2 * side_cap * sizeof(T) : 0;
-    const size_t side_off = (2 * grid_bytes + flag_bytes + trace_bytes + 511) & ~(size_t)255;
     {
       std::lock_guard<std::mutex> lk(g_mu);
-      int rc = arena_get(g_scratch[device & 15], side_off + 2 * side_bytes + 256, &scratch);
+      int rc = arena_get(g_scratch[device & 15], 2 * grid_bytes + flag_bytes + trace_bytes + 256,
+                         &scratch);
       if (rc) return rc;
     }
-    T* xsp0 = packed ? reinterpret_cast<T*>(reinterpret_cast<char*>(scratch) + side_off) : nullptr;
-    T* xsp1 = packed ? reinterpret_cast<T*>(reinterpret_cast<char*>(scratch) + side_off + side_bytes)
-                     : nullptr;
     T* xb0 = reinterpret_cast<T*>(scratch);
     T* xb1 = reinterpret_cast<T*>(reinterpret_cast<char*>(scratch) + grid_bytes);
     int* flags = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + 2 * grid_bytes);
@@ -1380,24 +1018,11 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
           reinterpret_cast<char*>(scratch) + ((2 * grid_bytes + flag_bytes + 255) & ~(size_t)255));
       CUDA_TRY(cudaMemsetAsync(trace, 0, trace_bytes, st));
     }
-    // stamped words: (ny + 2) x pitch values x WPV words, two parities
-    const size_t xs_bytes = (size_t)(ny + 2) * pitch * Stamped<T>::WPV * sizeof(uint64_t);
-    uint64_t* xs0 = nullptr;
-    uint32_t stamp0 = 0;
-    if (DTB_XCHG == 1 && !poison) {
-      std::lock_guard<std::mutex> lk(g_mu);
-      int rc = stamped_get(g_stamped[device & 15], 2 * xs_bytes, (steps + p.h - 1) / p.h, st,
-                           &xs0, &stamp0);
-      if (rc) return rc;
-    }
-    uint64_t* xs1 = xs0 ? xs0 + xs_bytes / sizeof(uint64_t) : nullptr;
     int h = p.h;
     int pois = poison ? 1 : 0;
-    void* args[] = {(void*)&d_in, (void*)&d_out, (void*)&xb0, (void*)&xb1, (void*)&xs0,
-                    (void*)&xs1, (void*)&stamp0, (void*)&flags,
+    void* args[] = {(void*)&d_in, (void*)&d_out, (void*)&xb0, (void*)&xb1, (void*)&flags,
                     (void*)&pitch, (void*)&nx, (void*)&ny, (void*)&wt, (void*)&steps,
-                    (void*)&h, (void*)&pois, (void*)&bs_on, (void*)&xsp0, (void*)&xsp1,
-                    (void*)&side_cap, (void*)&trace, (void*)&geo};
+                    (void*)&h, (void*)&pois, (void*)&bs_on, (void*)&trace, (void*)&geo};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(p.ctas), dim3(threads), args,
                                          (size_t)smem_res, st));
     g_launches += 1;
