@@ -1426,6 +1426,22 @@ int dtb_plan(int64_t nx, int64_t ny, int32_t elem_bytes, int64_t total_steps, in
 
 int64_t dtb_last_launch_count(void) { return g_launches; }
 
+// debug builds (DTB_PIPE_PROBE): per pipe stage {wait_in, wait_out, total} SM cycles,
+// summed over warps since the last call; resets the counters
+extern "C" int dtb_debug_pipe_probe(uint64_t* out) {
+#if DTB_PIPE_PROBE
+  unsigned long long h[8][3];
+  if (cudaMemcpyFromSymbol(h, dtb::g_pipe_probe, sizeof h) != cudaSuccess) return DTB_ECUDA;
+  for (int i = 0; i < 24; ++i) out[i] = (&h[0][0])[i];
+  unsigned long long z[8][3] = {};
+  if (cudaMemcpyToSymbol(dtb::g_pipe_probe, z, sizeof z) != cudaSuccess) return DTB_ECUDA;
+  return DTB_OK;
+#else
+  (void)out;
+  return DTB_EINVAL;
+#endif
+}
+
 int64_t dtb_last_trace(int64_t* out, int64_t n) {
   const int64_t m = std::min<int64_t>(n, (int64_t)g_trace.size());
   for (int64_t i = 0; i < m && out; ++i) out[i] = g_trace[(size_t)i];

@@ -82,6 +82,12 @@ struct PipeTile {
 #ifndef DTB_PIPE_NOINLINE
 #define DTB_PIPE_NOINLINE 0
 #endif
+#ifndef DTB_PIPE_PROBE
+#define DTB_PIPE_PROBE 0  // per-stage wait-cycle counters (dtb_debug_pipe_probe)
+#endif
+#if DTB_PIPE_PROBE
+__device__ unsigned long long g_pipe_probe[8][3];
+#endif
 #if DTB_PIPE_NOINLINE
 #define DTB_PIPE_INL __noinline__
 #else
@@ -146,8 +152,17 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
 #ifndef DTB_PIPE_POLL
 #define DTB_PIPE_POLL 1  // 1: every lane polls (warp-uniform loop); 0: lane 0 polls + syncwarp
 #endif
+#if DTB_PIPE_PROBE
+  unsigned long long w_in = 0, w_out = 0, t_all = clock64();
+#define DTB_PROBE_T0 const unsigned long long tp0_ = clock64();
+#define DTB_PROBE_ACC(v) v += clock64() - tp0_;
+#else
+#define DTB_PROBE_T0
+#define DTB_PROBE_ACC(v)
+#endif
   auto wait_in = [&](int q_hi) {
     if (!first) {
+      DTB_PROBE_T0
       if (DTB_PIPE_POLL) {
         while (ld_acquire_cta(prod + stage) < seq0 + q_hi + 1) __nanosleep(DTB_PIPE_SLEEP);
       } else {
@@ -155,6 +170,7 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
           while (ld_acquire_cta(prod + stage) < seq0 + q_hi + 1) __nanosleep(DTB_PIPE_SLEEP);
         __syncwarp();
       }
+      DTB_PROBE_ACC(w_in)
     }
   };
   auto release_in = [&](int q_done) {  // input rows < q_done fully read
@@ -165,6 +181,7 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
   };
   auto wait_out = [&](int q_hi) {
     if (!lastst) {
+      DTB_PROBE_T0
       if (DTB_PIPE_POLL) {
         while (ld_acquire_cta(cons + stage + 1) < seq0 + q_hi - kRingRows + 1) __nanosleep(DTB_PIPE_SLEEP);
       } else {
@@ -172,6 +189,7 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
           while (ld_acquire_cta(cons + stage + 1) < seq0 + q_hi - kRingRows + 1) __nanosleep(DTB_PIPE_SLEEP);
         __syncwarp();
       }
+      DTB_PROBE_ACC(w_out)
     }
   };
   auto release_out = [&](int q_done) {  // output rows < q_done written
@@ -307,18 +325,24 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
       uint32_t out_a = ring_out + (uint32_t)((seq0 + r - 2) % kRingRows) * RB;
       uint32_t pf_a = ring_in + (uint32_t)((seq0 + r + 2 + kPrefetch) % RIN) * RB;
       const T* pf_g = src + (int64_t)(pt.gy0 + r + 2 + kPrefetch) * pitch + pt.gx0;
+      const bool pf_fast = sizeof(T) == 8 && pt.vec && pt.Lw == L::ROW;  // fp32: slower (B200 A/B)
       T* st_g = dst + (int64_t)(pt.gy0 + r - 2) * pitch + pt.gx0 + c_lo;
 #define DTB_PIPE_SPEC_ROW(TM1, TC, TP1, TP2, BR, BM1, BM2, BM3)                   \
   {                                                                               \
     if constexpr (RL == 0) {                                                      \
       if (r + 2 + kPrefetch < Lh) {                                               \
-        _Pragma("unroll") for (int j = 0; j < CH; ++j) {                          \
-          const int cb = (lane * CH + j) * E;                                     \
-          if (pt.vec && cb + E <= pt.Lw) {                                        \
-            pipe_cp_async16(pf_a + off[j], pf_g + cb);                            \
-          } else {                                                                \
-            _Pragma("unroll") for (int e = 0; e < E; ++e) if (cb + e < pt.Lw)     \
-                pipe_cp_async(pf_a + off[j] + (uint32_t)(e * sizeof(T)), pf_g + cb + e); \
+        if (pf_fast) {  /* full-width aligned strip: CH chunk copies, no checks */\
+          _Pragma("unroll") for (int j = 0; j < CH; ++j)                          \
+              pipe_cp_async16(pf_a + off[j], pf_g + (lane * CH + j) * E);         \
+        } else {                                                                  \
+          _Pragma("unroll") for (int j = 0; j < CH; ++j) {                        \
+            const int cb = (lane * CH + j) * E;                                   \
+            if (pt.vec && cb + E <= pt.Lw) {                                      \
+              pipe_cp_async16(pf_a + off[j], pf_g + cb);                          \
+            } else {                                                              \
+              _Pragma("unroll") for (int e = 0; e < E; ++e) if (cb + e < pt.Lw)   \
+                  pipe_cp_async(pf_a + off[j] + (uint32_t)(e * sizeof(T)), pf_g + cb + e); \
+            }                                                                     \
           }                                                                       \
         }                                                                         \
       }                                                                           \
@@ -401,6 +425,13 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
 #undef DTB_PIPE_ITER
 #undef DTB_PIPE_STEADY
   }
+#if DTB_PIPE_PROBE
+  if (lane == 0) {
+    atomicAdd(&g_pipe_probe[stage][0], w_in);
+    atomicAdd(&g_pipe_probe[stage][1], w_out);
+    atomicAdd(&g_pipe_probe[stage][2], clock64() - t_all);
+  }
+#endif
   if (first) pipe_wait_group<0>();  // drain empty tail groups
   if (!first && lane == 0) st_release_cta(cons + stage, seq0 + Lh);  // whole tile consumed
 }
