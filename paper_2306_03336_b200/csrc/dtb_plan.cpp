@@ -179,6 +179,9 @@ constexpr double kExchangeLatency = 3500.0;  // flag publish + neighbour poll (~
 bool plan_resident(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& dev,
                    int depth, Plan& best) {
   bool found = false;
+  const bool small_grid = nx * ny <= 1024 * 1024;
+  const char* mt = getenv("DTB_MAX_TILES");  // experiments: cap the resident tile count
+  const int max_tiles = mt ? atoi(mt) : 1 << 30;
   for (const Shape& sh : shapes_for(elem)) {
     const int K = sh.K, W = sh.warps;
     const int Lw_max = 32 * K;
@@ -192,7 +195,10 @@ bool plan_resident(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInf
         Split sx;
         if (!make_split((int)nx, ntx, h, K, Lw_max, ntx > 1 ? h : 1, sx, 0, 16 / elem)) continue;
         const int nty_max = (int)std::min<int64_t>(dev.sms / ntx, ny);
-        for (int nty = nty_max; nty >= std::max(1, nty_max - 2); --nty) {
+        // few-tile plans too: latency-bound small grids (C1) may prefer them
+        const int nty_lo = std::max(1, small_grid ? 1 : nty_max - 2);
+        for (int nty = nty_max; nty >= nty_lo; --nty) {
+          if (ntx * nty > max_tiles) continue;
           Split sy;
           // (L - 2) a multiple of 4 rows per band: the static sweep fast path
           if (!make_split((int)ny, nty, h, W <= 8 ? 4 * W : 4, maxRows, nty > 1 ? h : 1, sy, 2)) continue;
