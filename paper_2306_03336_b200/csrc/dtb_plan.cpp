@@ -179,7 +179,6 @@ constexpr double kExchangeLatency = 3500.0;  // flag publish + neighbour poll (~
 bool plan_resident(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& dev,
                    int depth, Plan& best) {
   bool found = false;
-  const bool small_grid = nx * ny <= 1024 * 1024;
   const char* mt = getenv("DTB_MAX_TILES");  // experiments: cap the resident tile count
   const int max_tiles = mt ? atoi(mt) : 1 << 30;
   for (const Shape& sh : shapes_for(elem)) {
@@ -195,8 +194,7 @@ bool plan_resident(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInf
         Split sx;
         if (!make_split((int)nx, ntx, h, K, Lw_max, ntx > 1 ? h : 1, sx, 0, 16 / elem)) continue;
         const int nty_max = (int)std::min<int64_t>(dev.sms / ntx, ny);
-        // few-tile plans too: latency-bound small grids (C1) may prefer them
-        const int nty_lo = std::max(1, small_grid ? 1 : nty_max - 2);
+        const int nty_lo = std::max(1, nty_max - 2);
         for (int nty = nty_max; nty >= nty_lo; --nty) {
           if (ntx * nty > max_tiles) continue;
           Split sy;
