@@ -601,7 +601,23 @@ __device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya,
     if (bs && warp > 0) bs_wait(bs->pre + warp - 1, bs->seq);  // rows ya, ya+1 read
     uint32_t rowp = la.row(ya + 2);
     int rr = ya + 2;
-    for (int blk = (H - 4) >> 2; blk > 0; --blk) {
+#ifndef DTB_UNROLL8
+#define DTB_UNROLL8 (sizeof(T) == 8)  // 8-row steady blocks: fp64 +1.5 %, fp32 -2 % (B200 A/B)
+#endif
+    int blk = (H - 4) >> 2;
+    if (DTB_UNROLL8) {
+      for (; blk >= 2; blk -= 2) {
+        DTB_STEADY(t3, t0, t1, t2, b3, b2, b1, b0)
+        DTB_STEADY(t0, t1, t2, t3, b0, b3, b2, b1)
+        DTB_STEADY(t1, t2, t3, t0, b1, b0, b3, b2)
+        DTB_STEADY(t2, t3, t0, t1, b2, b1, b0, b3)
+        DTB_STEADY(t3, t0, t1, t2, b3, b2, b1, b0)
+        DTB_STEADY(t0, t1, t2, t3, b0, b3, b2, b1)
+        DTB_STEADY(t1, t2, t3, t0, b1, b0, b3, b2)
+        DTB_STEADY(t2, t3, t0, t1, b2, b1, b0, b3)
+      }
+    }
+    for (; blk > 0; --blk) {
       DTB_STEADY(t3, t0, t1, t2, b3, b2, b1, b0)
       DTB_STEADY(t0, t1, t2, t3, b0, b3, b2, b1)
       DTB_STEADY(t1, t2, t3, t0, b1, b0, b3, b2)
