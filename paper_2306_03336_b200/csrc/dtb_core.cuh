@@ -605,6 +605,24 @@ __device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya,
 #define DTB_UNROLL8 (sizeof(T) == 8)  // 8-row steady blocks: fp64 +1.5 %, fp32 -2 % (B200 A/B)
 #endif
     int blk = (H - 4) >> 2;
+#ifndef DTB_UNROLL_X
+#define DTB_UNROLL_X 2  // fp64 16-row steady blocks first (+0.6 % on C2 over 8-row blocks)
+#endif
+    if (DTB_UNROLL8 && DTB_UNROLL_X > 1) {
+      for (; blk >= 2 * DTB_UNROLL_X; blk -= 2 * DTB_UNROLL_X) {
+#pragma unroll
+        for (int u = 0; u < DTB_UNROLL_X; ++u) {
+          DTB_STEADY(t3, t0, t1, t2, b3, b2, b1, b0)
+          DTB_STEADY(t0, t1, t2, t3, b0, b3, b2, b1)
+          DTB_STEADY(t1, t2, t3, t0, b1, b0, b3, b2)
+          DTB_STEADY(t2, t3, t0, t1, b2, b1, b0, b3)
+          DTB_STEADY(t3, t0, t1, t2, b3, b2, b1, b0)
+          DTB_STEADY(t0, t1, t2, t3, b0, b3, b2, b1)
+          DTB_STEADY(t1, t2, t3, t0, b1, b0, b3, b2)
+          DTB_STEADY(t2, t3, t0, t1, b2, b1, b0, b3)
+        }
+      }
+    }
     if (DTB_UNROLL8) {
       for (; blk >= 2; blk -= 2) {
         DTB_STEADY(t3, t0, t1, t2, b3, b2, b1, b0)
