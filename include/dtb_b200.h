@@ -146,6 +146,11 @@ int dtb_fill_random_rows_f64(double* d_out, int64_t nx, int64_t ny, int64_t pitc
 /* Last error message on this thread ("" if none). */
 const char* dtb_last_error(void);
 
+/* Debug builds only (-DDTB_PIPE_PROBE=1): per pipe stage s, out[3s..3s+2] =
+ * {cycles waiting for input rows, cycles waiting for ring space, total cycles}
+ * summed over warps since the last call (then reset). DTB_EINVAL otherwise. */
+int dtb_debug_pipe_probe(uint64_t* out);
+
 #ifdef __cplusplus
 }
 #endif
