@@ -95,6 +95,7 @@ _SIGNATURES = {
     "dtb_fill_random_rows_f64": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_uint64, c_double,
                                          c_int64, c_int64, c_void_p]),
     "dtb_last_error": (c_char_p, []),
+    "dtb_debug_pipe_probe": (c_int, [POINTER(c_uint64)]),
 }
 
 _lib = None
