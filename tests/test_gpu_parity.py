@@ -295,3 +295,34 @@ def test_randomized_shapes_every_mode():
                 assert "fit" in str(e) or "feasible" in str(e) or "resident" in str(e), e
                 continue
             assert same(out.data.astype(dt), want), (nx, ny, steps, dt, flags, depth)
+
+
+_KNOB_SCRIPT = r"""
+import sys
+sys.path[:0] = ['.', 'tests']
+from test_gpu_parity import _device_bitwise_vs_naive
+from paper_2306_03336_b200.planner import plan_b200
+for nx, ny, dt in ((1900, 1900, 'f64'), (2700, 2700, 'f32'), (700, 900, 'f64'), (1300, 600, 'f32')):
+    p = plan_b200(nx, ny, 8 if dt == 'f64' else 4, 12, 1)
+    ok = _device_bitwise_vs_naive(nx, ny, 12, dt, seed=nx)
+    print(nx, ny, dt, p.mode, p.warps, p.tiles_x * p.tiles_y, p.ctas, ok)
+"""
+
+
+@pytest.mark.parametrize("env", ["DTB_GROUPS=2", "DTB_MAX_TILES=37", "DTB_SHAPE=4,8"])
+def test_planner_experiment_knobs_stay_bitwise(env):
+    """The planner's experiment knobs (two 4-warp tiles per CTA, capped tile
+    counts that push resident shapes into the pipe, pinned shapes) select
+    other schedules; each must still be bitwise equal to the naive kernel."""
+    import os
+    import subprocess
+    import sys
+    key, val = env.split("=")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _KNOB_SCRIPT], cwd=root, capture_output=True,
+                       text=True, env={**os.environ, key: val}, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = r.stdout.strip().splitlines()
+    assert len(lines) == 4 and all(l.endswith("True") for l in lines), r.stdout
+    if key == "DTB_GROUPS":  # two tiles per CTA were really taken
+        assert all(int(l.split()[5]) == 2 * int(l.split()[6]) for l in lines), r.stdout
