@@ -12,7 +12,8 @@ import ctypes
 
 import numpy as np
 
-__all__ = ["splitmix64", "random_doubles", "random_interior", "fill_random_device"]
+__all__ = ["splitmix64", "random_doubles", "random_interior", "Xoshiro256StarStar",
+           "fill_random_device"]
 
 _GOLDEN = np.uint64(0x9E3779B97F4B7C15)
 _M1 = np.uint64(0xBF58476D1CE4E5B9)
@@ -34,6 +35,48 @@ def random_doubles(seed: int, n: int) -> np.ndarray:
 
 def random_interior(nx: int, ny: int, seed: int) -> np.ndarray:
     return random_doubles(seed, nx * ny).reshape(ny, nx)
+
+
+class Xoshiro256StarStar:
+    """Sequential xoshiro256** stream whose four state words are the first four
+    splitmix64 outputs of ``seed`` (prng.py:74-111); the reference's tests and
+    acceptance batch draw their configurations from it."""
+
+    _M = (1 << 64) - 1
+
+    def __init__(self, seed: int):
+        self._s = [int(v) for v in splitmix64(seed, 4)]
+
+    @classmethod
+    def _rotl(cls, x: int, k: int) -> int:
+        return ((x << k) | (x >> (64 - k))) & cls._M
+
+    def next_u64(self) -> int:
+        a, b, c, d = self._s
+        out = (self._rotl((b * 5) & self._M, 7) * 9) & self._M
+        t = (b << 17) & self._M
+        c ^= a
+        d ^= b
+        b ^= c
+        a ^= d
+        self._s = [a, b, c ^ t, self._rotl(d, 45)]
+        return out
+
+    def random(self) -> float:
+        """Uniform double in [0, 1)."""
+        return (self.next_u64() >> 11) * (2.0 ** -53)
+
+    def uniform(self, lo: float, hi: float) -> float:
+        return lo + (hi - lo) * self.random()
+
+    def randint(self, lo: int, hi: int) -> int:
+        """Uniform integer in [lo, hi] (inclusive)."""
+        if hi < lo:
+            raise ValueError("empty range")
+        return lo + self.next_u64() % (hi - lo + 1)
+
+    def choice(self, seq):
+        return seq[self.randint(0, len(seq) - 1)]
 
 
 def fill_random_device(buf, nx: int, ny: int, seed: int, ghost: float = 0.0, stream=None):
