@@ -41,7 +41,7 @@ res = N["resident_kernel<double,4,8,0>"]
 pip = N["pipe_kernel<double,4,16,4,0>"]
 rewrite(os.path.join(ROOT, "profiles", "README.md"), [
     ("| **C2** fp64", f"| **C2** fp64 1900², 10⁴ steps (headline) | resident, h=4, 16×9 tiles of 128×226, 8 warps | **{v('c2'):.1f}** | {e('c2'):.1f} | smem {fr('c2','smem'):.3f} (16 B/cell vs 34.8 TB/s LDS.128), FP64 pipe {fr('c2','fp_pipe'):.3f} |"),
-    ("| C1 fp64", f"| C1 fp64 256², 100 steps | resident (138 tiles, h=10) | {v('c1'):.1f} | {e('c1'):.1f} | latency-floored: ~1.5 µs per step for any tiling (`DTB_MAX_TILES` sweep) |"),
+    ("| C1 fp64", f"| C1 fp64 256², 100 steps | resident (138 tiles, h=10) | {v('c1'):.1f} | {e('c1'):.1f} | latency-floored: ~1.25 µs per step for any tiling (`DTB_MAX_TILES` sweep); per the phase trace each two-step sweep costs ~2,000 cycles of ramp (pre-read, barrier, register-pipeline fill and drain) on top of ~200 cycles per band row, and C1's bands are 4 rows |"),
     ("| C3a fp32", f"| C3a fp32 2700², 10⁴ steps | resident, 11×13 tiles of 256×226 | {v('c3a'):.1f} | {e('c3a'):.1f} | smem {fr('c3a','smem'):.3f}, FP32 pipe {fr('c3a','fp_pipe'):.3f} |"),
     ("| C3b fp32", f"| C3b fp32 8192², 10³ steps | pipe, h=8, 35×16 segments | {v('c3b'):.1f} | {e('c3b'):.1f} | FP32 pipe {fr('c3b','fp_pipe'):.3f}, HBM {fr('c3b','hbm'):.3f} |"),
     ("| C4 fp64", f"| C4 fp64 16384², 10³ steps | pipe, h=8, 147×4 segments | {v('c4'):.1f} | {e('c4'):.1f} | FP64 pipe {fr('c4','fp_pipe'):.3f}, HBM {fr('c4','hbm'):.3f} |"),
@@ -53,7 +53,7 @@ rewrite(os.path.join(ROOT, "profiles", "README.md"), [
 ])
 rewrite(os.path.join(ROOT, "DESIGN.md"), [
     ("| C2 fp64 1900² ×10⁴ (headline)", f"| C2 fp64 1900² ×10⁴ (headline) | {v('c2'):.1f} (e2e {e('c2'):.1f}) | {fr('c2','fp_pipe'):.2f} (smem roofline {fr('c2','smem'):.2f}) | resident; h=4 forced by capacity, exchange every 4 steps |"),
-    ("| C1 fp64 256² ×100", f"| C1 fp64 256² ×100 | {v('c1'):.1f} (e2e {e('c1'):.1f}) | {fr('c1','fp_pipe'):.2f} | resident; ~1.5 µs per step latency floor |"),
+    ("| C1 fp64 256² ×100", f"| C1 fp64 256² ×100 | {v('c1'):.1f} (e2e {e('c1'):.1f}) | {fr('c1','fp_pipe'):.2f} | resident; latency floor: each two-step band sweep has a ~2,000-cycle ramp (pre-read, barrier, pipeline fill/drain) however few rows a band has, ~1.25 µs per step for any tiling |"),
     ("| C3a fp32 2700² ×10⁴", f"| C3a fp32 2700² ×10⁴ | {v('c3a'):.1f} | {fr('c3a','fp_pipe'):.2f} | resident |"),
     ("| C3b fp32 8192² ×10³", f"| C3b fp32 8192² ×10³ | {v('c3b'):.1f} | {fr('c3b','fp_pipe'):.2f} | pipe |"),
     ("| C4 fp64 16384² ×10³", f"| C4 fp64 16384² ×10³ | {v('c4'):.1f} | {fr('c4','fp_pipe'):.2f} | pipe |"),
