@@ -86,11 +86,15 @@ typedef struct dtb_plan_info {
   double est_cells_per_clk;               /* planner cost model */
 } dtb_plan_info;
 
-/* Host-buffer entry points (H2D + solve + D2H). n_gpus >= 1; t_depth >= 1 is
- * the reference plan's depth: total_steps must be a positive multiple of it
+/* Host-buffer entry points (H2D + solve + D2H). t_depth >= 1 is the
+ * reference plan's depth: total_steps must be a positive multiple of it
  * (engine.py:238-240). valid may be NULL (whole interior). ilp is accepted for
  * API parity (KernelConfig, kernel.py:33-41) and must be >= 1; it cannot
- * change results. rep may be NULL. */
+ * change results. rep may be NULL. n_gpus >= 1: with n_gpus > 1 the library
+ * splits the grid into n_gpus y-slabs over the visible devices (round-robin;
+ * slabs share a device when fewer are visible), exchanging 16-row halos by
+ * device-to-device copies (NVLink P2P) — bitwise equal to n_gpus = 1; not
+ * combinable with a valid region. The call stays blocking. */
 int dtb_j2d5pt_f64(const double* in, double* out, int64_t nx, int64_t ny, int64_t pitch,
                    const double w[5], int64_t total_steps, int64_t t_depth,
                    const dtb_rect* valid, int ilp, int n_gpus, unsigned flags,

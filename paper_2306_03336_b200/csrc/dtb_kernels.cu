@@ -1302,13 +1302,177 @@ int solve_dev(const T* d_in, T* d_out, int64_t nx, int64_t ny, int64_t pitch, co
   return DTB_OK;
 }
 
+// ---------------------------------------------------------------------------
+// n_gpus > 1 from the host entry: y-slabs (the native twin of
+// slab.py). Slab g owns interior rows [y0, y1) and keeps a local padded grid
+// of those rows plus kSlabDepth halo rows towards each neighbour (the global
+// ghost row on the outer sides). Every epoch of s <= depth steps each slab
+// advances its local grid s steps with its outer rows frozen (the trapezoid
+// argument: owned rows stay exact), then receives depth rows from each
+// neighbour into its halo by a device-to-device copy (P2P over NVLink when
+// the slabs sit on different GPUs). Slabs go round-robin over the visible
+// devices; slabs sharing a device run in order on that device's stream, so
+// no kernel ever waits on another's. Bitwise equal to n_gpus = 1.
+// ---------------------------------------------------------------------------
+constexpr int kSlabDepth = 16;
+
+struct DevBuffers {
+  std::vector<std::pair<int, void*>> bufs;  // (device, pointer)
+  std::vector<std::pair<int, cudaStream_t>> streams;
+  std::vector<cudaEvent_t> events;
+  int home = -1;  // the caller's device, restored on exit
+  ~DevBuffers() {
+    for (auto& s : streams) { cudaSetDevice(s.first); cudaStreamSynchronize(s.second); }
+    for (auto& e : events) cudaEventDestroy(e);
+    for (auto& s : streams) { cudaSetDevice(s.first); cudaStreamDestroy(s.second); }
+    for (auto& b : bufs) { cudaSetDevice(b.first); cudaFree(b.second); }
+    if (home >= 0) cudaSetDevice(home);
+  }
+};
+
+template <typename T>
+int solve_host_slabs(const T* in, T* out, int64_t nx, int64_t ny, int64_t pitch, const T w[5],
+                     int64_t total_steps, unsigned flags, int n_slabs, dtb_report* rep) {
+  if (ny < n_slabs)
+    return fail(DTB_EINVAL, "%lld rows cannot be split over %d GPUs", (long long)ny, n_slabs);
+  int ndev = 0, dev0 = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  CUDA_TRY(cudaGetDevice(&dev0));
+  if (ndev < 1) return fail(DTB_ECUDA, "no CUDA device");
+  const int64_t base = ny / n_slabs, rem = ny % n_slabs;
+  const int depth = (int)std::min<int64_t>(kSlabDepth, base);
+  struct Slab { int dev; int64_t y0, own, ht, hb, lny, row0; T* a; T* b; };
+  std::vector<Slab> sl(n_slabs);
+  const int64_t dpitch = (nx + 2 + 31) / 32 * 32;
+  const size_t hrow = (size_t)(nx + 2) * sizeof(T), drow = (size_t)dpitch * sizeof(T);
+  DevBuffers res;
+  res.home = dev0;
+  std::vector<cudaStream_t> dstream(std::min(ndev, n_slabs));
+  for (int d = 0; d < (int)dstream.size(); ++d) {
+    CUDA_TRY(cudaSetDevice((dev0 + d) % ndev));
+    CUDA_TRY(cudaStreamCreateWithFlags(&dstream[d], cudaStreamNonBlocking));
+    res.streams.push_back({(dev0 + d) % ndev, dstream[d]});
+    for (int e = 0; e < (int)dstream.size(); ++e)  // best effort: direct NVLink copies
+      if (e != d && cudaDeviceEnablePeerAccess((dev0 + e) % ndev, 0) != cudaSuccess)
+        cudaGetLastError();
+  }
+  int64_t y = 0;
+  for (int g = 0; g < n_slabs; ++g) {
+    Slab& s = sl[g];
+    s.dev = g % (int)dstream.size();
+    s.y0 = y;
+    s.own = base + (g < rem ? 1 : 0);
+    y += s.own;
+    s.ht = g > 0 ? depth : 1;
+    s.hb = g + 1 < n_slabs ? depth : 1;
+    s.lny = s.own + s.ht + s.hb - 2;
+    s.row0 = s.y0 + 1 - s.ht;  // padded global row of local row 0
+    const size_t bytes = (size_t)(s.lny + 2) * drow;
+    CUDA_TRY(cudaSetDevice((dev0 + s.dev) % ndev));
+    void* p = nullptr;
+    CUDA_TRY(cudaMalloc(&p, 2 * bytes));
+    res.bufs.push_back({(dev0 + s.dev) % ndev, p});
+    s.a = reinterpret_cast<T*>(p);
+    s.b = reinterpret_cast<T*>(reinterpret_cast<char*>(p) + bytes);
+    CUDA_TRY(cudaMemcpy2DAsync(s.a, drow, in + s.row0 * pitch, pitch * sizeof(T), hrow,
+                               s.lny + 2, cudaMemcpyHostToDevice, dstream[s.dev]));
+  }
+  std::vector<cudaEvent_t> solved(n_slabs), copied(n_slabs);
+  for (int g = 0; g < n_slabs; ++g) {
+    CUDA_TRY(cudaSetDevice((dev0 + sl[g].dev) % ndev));
+    CUDA_TRY(cudaEventCreateWithFlags(&solved[g], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&copied[g], cudaEventDisableTiming));
+    res.events.push_back(solved[g]);
+    res.events.push_back(copied[g]);
+  }
+  dtb_report acc;
+  memset(&acc, 0, sizeof acc);
+  int64_t launches = 0, done = 0;
+  const unsigned lflags = flags & ~(unsigned)DTB_FLAG_FORCE_DEPTH;
+  while (done < total_steps) {
+    const int64_t s_ep = std::min<int64_t>(depth, total_steps - done);
+    for (int g = 0; g < n_slabs; ++g) {
+      Slab& s = sl[g];
+      cudaStream_t st = dstream[s.dev];
+      CUDA_TRY(cudaSetDevice((dev0 + s.dev) % ndev));
+      // the neighbours' last reads of our previous result buffer (their halo copies) are done
+      if (done > 0) {
+        if (g > 0) CUDA_TRY(cudaStreamWaitEvent(st, copied[g - 1], 0));
+        if (g + 1 < n_slabs) CUDA_TRY(cudaStreamWaitEvent(st, copied[g + 1], 0));
+      }
+      dtb_report r;
+      if (int rc = solve_dev<T>(s.a, s.b, nx, s.lny, dpitch, w, s_ep, 1, nullptr, lflags, st, &r))
+        return rc;
+      launches += g_launches;
+      acc.global_load_cells += r.global_load_cells;
+      acc.global_store_cells += r.global_store_cells;
+      acc.redundant_compute_cells += r.redundant_compute_cells + r.useful_compute_cells;
+      acc.scratchpad_peak_bytes = std::max(acc.scratchpad_peak_bytes, r.scratchpad_peak_bytes);
+      std::swap(s.a, s.b);
+      CUDA_TRY(cudaEventRecord(solved[g], st));
+    }
+    done += s_ep;
+    if (done >= total_steps) break;
+    for (int g = 0; g < n_slabs; ++g) {  // halo rows from each neighbour's owned edge rows
+      Slab& s = sl[g];
+      cudaStream_t st = dstream[s.dev];
+      CUDA_TRY(cudaSetDevice((dev0 + s.dev) % ndev));
+      if (g > 0) {
+        const Slab& u = sl[g - 1];
+        CUDA_TRY(cudaStreamWaitEvent(st, solved[g - 1], 0));
+        CUDA_TRY(cudaMemcpy2DAsync(s.a, drow, u.a + (u.ht + u.own - depth) * dpitch, drow, hrow,
+                                   depth, cudaMemcpyDefault, st));
+        acc.halo_exchanged_cells += depth * nx;
+      }
+      if (g + 1 < n_slabs) {
+        const Slab& d = sl[g + 1];
+        CUDA_TRY(cudaStreamWaitEvent(st, solved[g + 1], 0));
+        CUDA_TRY(cudaMemcpy2DAsync(s.a + (s.ht + s.own) * dpitch, drow, d.a + d.ht * dpitch, drow,
+                                   hrow, depth, cudaMemcpyDefault, st));
+        acc.halo_exchanged_cells += depth * nx;
+      }
+      CUDA_TRY(cudaEventRecord(copied[g], st));
+    }
+  }
+  for (int g = 0; g < n_slabs; ++g) {  // owned rows (and the global ghost rows) back
+    const Slab& s = sl[g];
+    CUDA_TRY(cudaSetDevice((dev0 + s.dev) % ndev));
+    const int64_t r0 = g == 0 ? 0 : s.ht, r1 = s.ht + s.own + (g + 1 == n_slabs ? 1 : 0);
+    CUDA_TRY(cudaMemcpy2DAsync(out + (s.row0 + r0) * pitch, pitch * sizeof(T), s.a + r0 * dpitch,
+                               drow, hrow, r1 - r0, cudaMemcpyDeviceToHost, dstream[s.dev]));
+  }
+  for (int d = 0; d < (int)dstream.size(); ++d) {
+    CUDA_TRY(cudaSetDevice((dev0 + d) % ndev));
+    CUDA_TRY(cudaStreamSynchronize(dstream[d]));
+  }
+  g_launches = launches;
+  if (rep) {
+    *rep = acc;
+    rep->elem_bytes = (int64_t)sizeof(T);
+    rep->useful_compute_cells = nx * ny * total_steps;
+    rep->redundant_compute_cells -= rep->useful_compute_cells;
+  }
+  return DTB_OK;
+}
+
 template <typename T>
 int solve_host(const T* in, T* out, int64_t nx, int64_t ny, int64_t pitch, const T w[5],
                int64_t total_steps, int64_t t_depth, const dtb_rect* valid, int ilp, int n_gpus,
                unsigned flags, dtb_report* rep) {
   if (!in || !out) return fail(DTB_EINVAL, "null buffer");
   if (ilp < 1) return fail(DTB_EINVAL, "ilp must be at least 1, got %d", ilp);
-  if (n_gpus != 1) return fail(DTB_EINVAL, "n_gpus=%d: the host entry point drives one GPU; use the slab API for more", n_gpus);
+  if (n_gpus < 1) return fail(DTB_EINVAL, "n_gpus must be at least 1, got %d", n_gpus);
+  if (n_gpus > 1) {
+    double wd[5];
+    for (int i = 0; i < 5; ++i) wd[i] = (double)w[i];
+    if (int rc = validate(nx, ny, pitch, wd, total_steps,
+                          (flags & DTB_FLAG_FORCE_DEPTH) ? 1 : t_depth, valid))
+      return rc;
+    if (valid && !(valid->x0 == 0 && valid->y0 == 0 && valid->width == nx && valid->height == ny))
+      return fail(DTB_EINVAL, "a valid= region needs n_gpus = 1");
+    g_err.clear();
+    return solve_host_slabs<T>(in, out, nx, ny, pitch, w, total_steps, flags, n_gpus, rep);
+  }
   double wd[5];
   for (int i = 0; i < 5; ++i) wd[i] = (double)w[i];
   int rc = validate(nx, ny, pitch, wd, total_steps,

@@ -92,7 +92,8 @@ def _check_valid(nx: int, ny: int, valid):
 
 
 def _solve_host(data: np.ndarray, nx: int, ny: int, weights, steps: int, t_depth: int,
-                valid, ilp: int, flags: int, dtype) -> tuple[np.ndarray, _native.DtbReport]:
+                valid, ilp: int, flags: int, dtype, n_gpus: int = 1
+                ) -> tuple[np.ndarray, _native.DtbReport]:
     dt = np.dtype(dtype)
     if dt not in _DTYPES:
         raise ValueError(f"dtype must be float64 or float32, got {dt}")
@@ -104,7 +105,7 @@ def _solve_host(data: np.ndarray, nx: int, ny: int, weights, steps: int, t_depth
     vr = _rect(valid)
     fn = getattr(_native.lib(), f"dtb_j2d5pt_{tag}")
     rc = fn(src.ctypes.data, out.ctypes.data, nx, ny, nx + 2, w, steps, t_depth,
-            ctypes.byref(vr) if vr is not None else None, ilp, 1, flags, ctypes.byref(rep))
+            ctypes.byref(vr) if vr is not None else None, ilp, n_gpus, flags, ctypes.byref(rep))
     if rc != _native.DTB_OK:
         _raise(rc)
     return out, rep
@@ -150,17 +151,18 @@ def run_dtb(grid, weights, total_steps: int, plan=None, cfg: KernelConfig = Kern
 
 
 def run_dtb_b200(grid, weights, total_steps: int, *, valid=None, poison: bool = False,
-                 dtype=np.float64, flags: int = 0, depth: int | None = None
+                 dtype=np.float64, flags: int = 0, depth: int | None = None, n_gpus: int = 1
                  ) -> tuple[Grid2D, TrafficReport]:
     """Like run_dtb without a reference plan, returning the B200 schedule's own
     traffic (dtb_report). ``flags`` takes _native.FLAG_FORCE_* for tests;
-    ``depth`` pins the temporal halo depth."""
+    ``depth`` pins the temporal halo depth; ``n_gpus`` > 1 splits the grid
+    into y-slabs over the visible GPUs inside the library (one process)."""
     _check_valid(grid.nx, grid.ny, valid)
     if depth is not None:
         flags |= _native.FLAG_FORCE_DEPTH
     out, rep = _solve_host(grid.data, grid.nx, grid.ny, weights, total_steps,
                            depth if depth is not None else 1, valid, 1,
-                           flags | (_native.FLAG_POISON if poison else 0), dtype)
+                           flags | (_native.FLAG_POISON if poison else 0), dtype, n_gpus)
     return Grid2D(grid.nx, grid.ny, out.astype(np.float64)), _report(rep)
 
 
