@@ -50,6 +50,9 @@ extern "C" {
 #define DTB_FLAG_TRACE 16u          /* resident kernel: per-CTA clock64 phase counters (dtb_last_trace) */
 #define DTB_FLAG_FORCE_PIPE 32u     /* use the pipelined (warp-pipeline, column-strip) streaming kernel */
 #define DTB_FLAG_FORCE_RESIDENT 64u /* use the smem-resident kernel (fails if the grid does not fit) */
+#define DTB_FLAG_SLAB_COPY 128u     /* n_gpus > 1: exchange slab halos by copies after each epoch */
+#define DTB_FLAG_SLAB_FUSED 256u    /* n_gpus > 1: pipelined kernel on every slab, halos stored
+                                       into the neighbours in-kernel (fails if a slab cannot) */
 
 /* Half-open rectangle in interior coordinates (grid.py:38-92). */
 typedef struct dtb_rect {

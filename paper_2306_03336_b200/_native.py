@@ -28,6 +28,8 @@ FLAG_FORCE_DEPTH = 8
 FLAG_TRACE = 16
 FLAG_FORCE_PIPE = 32
 FLAG_FORCE_RESIDENT = 64
+FLAG_SLAB_COPY = 128
+FLAG_SLAB_FUSED = 256
 
 
 class DtbRect(ctypes.Structure):

@@ -523,10 +523,11 @@ struct PipeSmem {
   int prod[S], cons[S];
 };
 
-template <typename T, int K, int NW, int S, bool DYN>
+template <typename T, int K, int NW, int S, bool DYN, bool MIR = false>
 __global__ void __launch_bounds__(NW * 32, 1)
 pipe_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int nx, int ny,
-            Weights<T> wt, int steps, const __grid_constant__ Geometry geo) {
+            Weights<T> wt, int steps, const __grid_constant__ Geometry geo,
+            const __grid_constant__ HaloMirror<T> mir) {
   constexpr int P = NW / S;
   typedef Tile<T, K> L;
   constexpr int RB = L::ROW * (int)sizeof(T);
@@ -569,11 +570,17 @@ pipe_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int n
     pt.ox1 = cx.y + (cx.y == nx) - cx.z;
     pt.oy0 = cy.x - (cy.x == 0) - cy.z;
     pt.oy1 = cy.y + (cy.y == ny) - cy.z;
+    pt.qy0 = pt.oy0;
+    pt.qy1 = pt.oy1;
+    if (MIR) {  // own stores only inside the window; the neighbours fill the rest
+      pt.oy0 = max(pt.oy0, (int)(mir.sw0 - pt.gy0));
+      pt.oy1 = min(pt.oy1, (int)(mir.sw1 - pt.gy0));
+    }
     pt.vec = ((pt.gx0 % L::EPC) == 0) && ((pitch % L::EPC) == 0);
     lc.last = lc.lane == (pt.Lw - 1) / K;
     lc.last_e = (pt.Lw - 1) % K;
-    pipe_stage<T, K, NW, DYN>(pt, s, S, levels, seq, src, dst, pitch, ring_in, ring_out,
-                          ctl[p].prod, ctl[p].cons, wt, lc);
+    pipe_stage<T, K, NW, DYN, MIR>(pt, s, S, levels, seq, src, dst, pitch, ring_in, ring_out,
+                               ctl[p].prod, ctl[p].cons, wt, lc, &mir);
     seq += pt.Lh;
   }
 }
@@ -835,6 +842,9 @@ using namespace dtb;
 
 thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
+// set by solve_host_slabs around one slab's solve: the pipe kernel's final
+// pass then feeds the neighbour slabs' halos in-kernel (HaloMirror)
+thread_local const void* g_halo_mirror = nullptr;
 thread_local std::vector<int64_t> g_trace;
 thread_local unsigned g_flags = 0;
 
@@ -1109,12 +1119,23 @@ int launch_pipe(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int
   DevInfo di;
   if (int rc = query_dev(di)) return rc;
   const int ctas = (int)std::min<int64_t>(di.sms, (ntiles + P - 1) / P);
+  const HaloMirror<T>* mir = static_cast<const HaloMirror<T>*>(g_halo_mirror);
+  HaloMirror<T> none;
+  memset(&none, 0, sizeof none);
+  if (mir) {
+    auto kmir = pipe_kernel<T, K, PW, S, DYN, true>;
+    if (int rc = prepare_kernel((const void*)kmir, device, psmem, PW * 32, nullptr)) return rc;
+  }
   const T* src = d_in;
   int64_t done = 0;
   for (int64_t i = 0; i < passes; ++i) {
     const int s = (int)std::min<int64_t>(2 * S, steps - done);
     T* dst = ((passes - 1 - i) % 2 == 0) ? d_out : tmp;
-    kern<<<ctas, PW * 32, psmem, st>>>(src, dst, pitch, nx, ny, wt, s, geo);
+    if (mir && i + 1 == passes)  // the epoch's result: also feed the neighbours' halos
+      pipe_kernel<T, K, PW, S, DYN, true><<<ctas, PW * 32, psmem, st>>>(src, dst, pitch, nx, ny,
+                                                                         wt, s, geo, *mir);
+    else
+      kern<<<ctas, PW * 32, psmem, st>>>(src, dst, pitch, nx, ny, wt, s, geo, none);
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
     src = dst;
@@ -1143,6 +1164,8 @@ int dispatch(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_
     return p.dyn() ? launch_pipe<T, KK, DTB_PIPE_WARPS, true>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, st)
                    : launch_pipe<T, KK, DTB_PIPE_WARPS, false>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, st);
   }
+  if (g_halo_mirror)
+    return fail(DTB_EINVAL, "fused slab halos need the pipelined kernel (plan mode %d)", p.mode);
 #define DTB_SHAPE(KK, WW)                                                                  \
   if (p.K == KK && p.warps == WW && p.groups == 1)                                         \
     return dispatch_dyn<T, KK, WW>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st);
@@ -1377,56 +1400,118 @@ int solve_host_slabs(const T* in, T* out, int64_t nx, int64_t ny, int64_t pitch,
     CUDA_TRY(cudaMemcpy2DAsync(s.a, drow, in + s.row0 * pitch, pitch * sizeof(T), hrow,
                                s.lny + 2, cudaMemcpyHostToDevice, dstream[s.dev]));
   }
-  std::vector<cudaEvent_t> solved(n_slabs), copied(n_slabs);
+  // exchange mode: fused (the pipe kernel's final pass of each epoch stores
+  // the neighbours' halo rows straight into their next input, P2P when they
+  // live on another GPU) whenever every slab runs the pipelined kernel; else
+  // device-to-device copies after each epoch
+  bool fused = (flags & DTB_FLAG_SLAB_COPY) == 0 && n_slabs > 1;
+  if (fused) {
+    DevInfo di;
+    if (int rc = query_dev(di)) return rc;
+    const int force = (flags & DTB_FLAG_SLAB_FUSED) ? 3 : 0;
+    for (int g = 0; g < n_slabs && fused; ++g) {
+      Plan p;
+      char err[256];
+      fused = make_plan(nx, sl[g].lny, (int)sizeof(T), depth, di, force, 0, p, err, sizeof err) &&
+              p.mode == 3;
+    }
+  }
+  if ((flags & DTB_FLAG_SLAB_FUSED) && !fused)
+    return fail(DTB_EINFEASIBLE, "fused slab halos need the pipelined kernel on every slab");
+  std::vector<cudaEvent_t> solved(2 * n_slabs), copied(n_slabs);  // solved: epoch parity
   for (int g = 0; g < n_slabs; ++g) {
     CUDA_TRY(cudaSetDevice((dev0 + sl[g].dev) % ndev));
-    CUDA_TRY(cudaEventCreateWithFlags(&solved[g], cudaEventDisableTiming));
+    for (int k = 0; k < 2; ++k) {
+      CUDA_TRY(cudaEventCreateWithFlags(&solved[k * n_slabs + g], cudaEventDisableTiming));
+      res.events.push_back(solved[k * n_slabs + g]);
+    }
     CUDA_TRY(cudaEventCreateWithFlags(&copied[g], cudaEventDisableTiming));
-    res.events.push_back(solved[g]);
     res.events.push_back(copied[g]);
   }
+  struct MirrorScope {  // g_halo_mirror for exactly one slab solve
+    explicit MirrorScope(const void* m) { g_halo_mirror = m; }
+    ~MirrorScope() { g_halo_mirror = nullptr; }
+  };
   dtb_report acc;
   memset(&acc, 0, sizeof acc);
   int64_t launches = 0, done = 0;
-  const unsigned lflags = flags & ~(unsigned)DTB_FLAG_FORCE_DEPTH;
+  int epoch = 0;
+  const unsigned lflags = (flags & ~(unsigned)(DTB_FLAG_FORCE_DEPTH | DTB_FLAG_SLAB_COPY |
+                                                DTB_FLAG_SLAB_FUSED)) |
+                          (fused ? (unsigned)DTB_FLAG_FORCE_PIPE : 0u);
+  std::vector<T*> next(n_slabs);
   while (done < total_steps) {
     const int64_t s_ep = std::min<int64_t>(depth, total_steps - done);
+    const int cur = epoch & 1, prev = cur ^ 1;
+    for (int g = 0; g < n_slabs; ++g) next[g] = sl[g].b;  // this epoch's outputs
     for (int g = 0; g < n_slabs; ++g) {
       Slab& s = sl[g];
       cudaStream_t st = dstream[s.dev];
       CUDA_TRY(cudaSetDevice((dev0 + s.dev) % ndev));
-      // the neighbours' last reads of our previous result buffer (their halo copies) are done
-      if (done > 0) {
-        if (g > 0) CUDA_TRY(cudaStreamWaitEvent(st, copied[g - 1], 0));
-        if (g + 1 < n_slabs) CUDA_TRY(cudaStreamWaitEvent(st, copied[g + 1], 0));
+      if (epoch > 0) {
+        if (fused) {
+          // our halo rows in s.a came from the neighbours' previous epoch, and the
+          // buffers we are about to write into were read by that epoch
+          if (g > 0) CUDA_TRY(cudaStreamWaitEvent(st, solved[prev * n_slabs + g - 1], 0));
+          if (g + 1 < n_slabs) CUDA_TRY(cudaStreamWaitEvent(st, solved[prev * n_slabs + g + 1], 0));
+        } else {
+          // the neighbours' last reads of our previous result buffer (their halo copies) are done
+          if (g > 0) CUDA_TRY(cudaStreamWaitEvent(st, copied[g - 1], 0));
+          if (g + 1 < n_slabs) CUDA_TRY(cudaStreamWaitEvent(st, copied[g + 1], 0));
+        }
+      }
+      HaloMirror<T> m;
+      memset(&m, 0, sizeof m);
+      m.sw0 = g == 0 ? 0 : s.ht;
+      m.sw1 = g + 1 == n_slabs ? s.lny + 2 : s.ht + s.own;
+      if (g > 0) {  // our first owned rows -> the upper slab's bottom halo
+        const Slab& u = sl[g - 1];
+        m.peer[0] = next[g - 1];
+        m.r0[0] = s.ht;
+        m.r1[0] = s.ht + depth;
+        m.p0[0] = u.ht + u.own;
+      }
+      if (g + 1 < n_slabs) {  // our last owned rows -> the lower slab's top halo
+        m.peer[1] = next[g + 1];
+        m.r0[1] = s.ht + s.own - depth;
+        m.r1[1] = s.ht + s.own;
+        m.p0[1] = 0;
       }
       dtb_report r;
-      if (int rc = solve_dev<T>(s.a, s.b, nx, s.lny, dpitch, w, s_ep, 1, nullptr, lflags, st, &r))
-        return rc;
+      {
+        MirrorScope scope(fused ? &m : nullptr);
+        if (int rc = solve_dev<T>(s.a, s.b, nx, s.lny, dpitch, w, s_ep, 1, nullptr, lflags, st, &r))
+          return rc;
+      }
       launches += g_launches;
       acc.global_load_cells += r.global_load_cells;
       acc.global_store_cells += r.global_store_cells;
       acc.redundant_compute_cells += r.redundant_compute_cells + r.useful_compute_cells;
       acc.scratchpad_peak_bytes = std::max(acc.scratchpad_peak_bytes, r.scratchpad_peak_bytes);
       std::swap(s.a, s.b);
-      CUDA_TRY(cudaEventRecord(solved[g], st));
+      CUDA_TRY(cudaEventRecord(solved[cur * n_slabs + g], st));
     }
     done += s_ep;
+    ++epoch;
     if (done >= total_steps) break;
+    if (fused) {
+      acc.halo_exchanged_cells += 2 * (int64_t)(n_slabs - 1) * depth * nx;
+      continue;
+    }
     for (int g = 0; g < n_slabs; ++g) {  // halo rows from each neighbour's owned edge rows
       Slab& s = sl[g];
       cudaStream_t st = dstream[s.dev];
       CUDA_TRY(cudaSetDevice((dev0 + s.dev) % ndev));
       if (g > 0) {
         const Slab& u = sl[g - 1];
-        CUDA_TRY(cudaStreamWaitEvent(st, solved[g - 1], 0));
+        CUDA_TRY(cudaStreamWaitEvent(st, solved[cur * n_slabs + g - 1], 0));
         CUDA_TRY(cudaMemcpy2DAsync(s.a, drow, u.a + (u.ht + u.own - depth) * dpitch, drow, hrow,
                                    depth, cudaMemcpyDefault, st));
         acc.halo_exchanged_cells += depth * nx;
       }
       if (g + 1 < n_slabs) {
         const Slab& d = sl[g + 1];
-        CUDA_TRY(cudaStreamWaitEvent(st, solved[g + 1], 0));
+        CUDA_TRY(cudaStreamWaitEvent(st, solved[cur * n_slabs + g + 1], 0));
         CUDA_TRY(cudaMemcpy2DAsync(s.a + (s.ht + s.own) * dpitch, drow, d.a + d.ht * dpitch, drow,
                                    hrow, depth, cudaMemcpyDefault, st));
         acc.halo_exchanged_cells += depth * nx;

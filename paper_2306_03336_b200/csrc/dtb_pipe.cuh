@@ -65,11 +65,24 @@ struct PipeCfg {
   static constexpr int kPrefetch = NW >= 16 ? (kDeep ? DTB_PIPE_PF : 6) : 8;  // HBM rows in flight
 };
 
+// Fused slab halo exchange (n_gpus > 1 through the C ABI): the last stage
+// also stores padded rows [r0[i], r1[i]) of its output into a neighbour
+// slab's next input at rows p0[i].. (a peer GPU's buffer over NVLink, or the
+// same device when slabs share one), and stores its own rows only inside
+// [sw0, sw1) so it never touches the halo rows the neighbours write.
+template <typename T>
+struct HaloMirror {
+  T* peer[2];
+  int64_t r0[2], r1[2], p0[2];
+  int64_t sw0, sw1;
+};
+
 struct PipeTile {
   int Lw, Lh;        // load region (tile-local rows/cols)
   int gx0, gy0;      // padded global coords of tile (0,0)
   int ox0, ox1;      // store columns (owned, + ghost at domain edges), tile-local
   int oy0, oy1;      // store rows, tile-local
+  int qy0, qy1;      // owned rows, tile-local (oy before a HaloMirror store window)
   bool vec;          // global side 16-byte aligned per chunk
 };
 
@@ -93,13 +106,14 @@ __device__ unsigned long long g_pipe_probe[8][3];
 #else
 #define DTB_PIPE_INL __forceinline__
 #endif
-template <typename T, int K, int NW, bool DYN, int ROLE>
+template <typename T, int K, int NW, bool DYN, int ROLE, bool MIR = false>
 __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int levels,
                                                 int seq0, const T* __restrict__ src,
                                                 T* __restrict__ dst, int64_t pitch,
                                                 uint32_t ring_in, uint32_t ring_out, int* prod,
                                                 int* cons, const Weights<T>& wt,
-                                                const LaneCtx& lc, int nstages_) {
+                                                const LaneCtx& lc, int nstages_,
+                                                const HaloMirror<T>* mir = nullptr) {
   typedef Tile<T, K> L;
   constexpr int E = L::EPC, CH = L::CH;
   constexpr uint32_t RB = (uint32_t)(L::ROW * sizeof(T));  // bytes per ring row
@@ -216,8 +230,24 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
   // ---- output rows -------------------------------------------------------
   const int c_lo = lane * K;
   const bool full_vec = pt.vec && c_lo >= pt.ox0 && c_lo + K <= pt.ox1;
+  // fused slab exchange: rows the neighbours need next epoch go to them too
+  auto mirror_row = [&](int q, const T (&v)[K]) {
+    if constexpr (MIR) {
+      const int64_t gr = pt.gy0 + q;
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        if (q >= pt.qy0 && q < pt.qy1 && gr >= mir->r0[i] && gr < mir->r1[i]) {
+          T* g = mir->peer[i] + (gr - mir->r0[i] + mir->p0[i]) * pitch + pt.gx0 + c_lo;
+#pragma unroll
+          for (int e = 0; e < K; ++e)
+            if (c_lo + e >= pt.ox0 && c_lo + e < pt.ox1) g[e] = v[e];
+        }
+      }
+    }
+  };
   auto put_row_nosync = [&](int q, const T (&v)[K]) {
     if (lastst) {
+      if (MIR) mirror_row(q, v);
       if (q >= pt.oy0 && q < pt.oy1) {
         T* g = dst + (int64_t)(pt.gy0 + q) * pitch + pt.gx0 + c_lo;
         if (full_vec) {
@@ -362,6 +392,7 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
       row_update<T, K, DYN>(BM3, BM2, BM1, o, wt, lc);                            \
     }                                                                             \
     if constexpr (RL == 2) {                                                      \
+      if (MIR) mirror_row(r - 2, o);                                              \
       if (r - 2 >= pt.oy0 && r - 2 < pt.oy1) {                                    \
         if (full_vec) {                                                           \
           typedef typename Arith<T>::vec_t V;                                     \
@@ -436,21 +467,22 @@ __device__ DTB_PIPE_INL void pipe_stage_role(const PipeTile& pt, int stage, int 
   if (!first && lane == 0) st_release_cta(cons + stage, seq0 + Lh);  // whole tile consumed
 }
 
-template <typename T, int K, int NW, bool DYN>
+template <typename T, int K, int NW, bool DYN, bool MIR = false>
 __device__ __forceinline__ void pipe_stage(const PipeTile& pt, int stage, int nstages, int levels,
                                            int seq0, const T* __restrict__ src,
                                            T* __restrict__ dst, int64_t pitch, uint32_t ring_in,
                                            uint32_t ring_out, int* prod, int* cons,
-                                           const Weights<T>& wt, const LaneCtx& lc) {
+                                           const Weights<T>& wt, const LaneCtx& lc,
+                                           const HaloMirror<T>* mir = nullptr) {
   if (DTB_PIPE_ROLES && stage == 0)
-    pipe_stage_role<T, K, NW, DYN, 0>(pt, stage, levels, seq0, src, dst, pitch, ring_in,
-                                      ring_out, prod, cons, wt, lc, nstages);
+    pipe_stage_role<T, K, NW, DYN, 0, MIR>(pt, stage, levels, seq0, src, dst, pitch, ring_in,
+                                           ring_out, prod, cons, wt, lc, nstages, mir);
   else if (DTB_PIPE_ROLES && stage == nstages - 1)
-    pipe_stage_role<T, K, NW, DYN, 2>(pt, stage, levels, seq0, src, dst, pitch, ring_in,
-                                      ring_out, prod, cons, wt, lc, nstages);
+    pipe_stage_role<T, K, NW, DYN, 2, MIR>(pt, stage, levels, seq0, src, dst, pitch, ring_in,
+                                           ring_out, prod, cons, wt, lc, nstages, mir);
   else
-    pipe_stage_role<T, K, NW, DYN, 1>(pt, stage, levels, seq0, src, dst, pitch, ring_in,
-                                      ring_out, prod, cons, wt, lc, nstages);
+    pipe_stage_role<T, K, NW, DYN, 1, MIR>(pt, stage, levels, seq0, src, dst, pitch, ring_in,
+                                           ring_out, prod, cons, wt, lc, nstages, mir);
 }
 
 }  // namespace dtb

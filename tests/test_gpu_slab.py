@@ -65,3 +65,21 @@ def test_host_entry_n_gpus_slabs_bitwise(n_gpus, nx, ny, steps, dt):
     want = jacobi_c(g.data, w.astuple(), steps, dt)
     assert np.array_equal(multi.data.astype(dt), want)
     assert rep.useful_compute_cells == nx * ny * steps and rep.halo_exchanged_cells > 0
+
+
+@pytest.mark.parametrize("n_gpus,nx,ny,steps,dt", [
+    (2, 1000, 700, 40, np.float64), (3, 777, 1201, 33, np.float32), (4, 2048, 512, 48, np.float64)])
+def test_host_entry_fused_slab_halos_bitwise(n_gpus, nx, ny, steps, dt):
+    """Fused exchange: each slab's pipelined kernel stores the neighbours' halo
+    rows into their next input in-kernel (HaloMirror), its own stores limited
+    to its owned rows; bitwise equal to the copy exchange, one GPU and the oracle."""
+    from oracle import jacobi_c
+    from paper_2306_03336_b200 import StencilWeights, _native, grid_new, run_dtb_b200
+    from paper_2306_03336_b200.prng import random_interior
+    g = grid_new(nx, ny, random_interior(nx, ny, 7 * n_gpus), ghost=-1.5)
+    w = StencilWeights(0.11, -0.2, 0.37, 0.5, -0.07)
+    fused, rep = run_dtb_b200(g, w, steps, dtype=dt, n_gpus=n_gpus, flags=_native.FLAG_SLAB_FUSED)
+    copy, _ = run_dtb_b200(g, w, steps, dtype=dt, n_gpus=n_gpus, flags=_native.FLAG_SLAB_COPY)
+    assert np.array_equal(fused.data.view(np.uint64), copy.data.view(np.uint64))
+    assert np.array_equal(fused.data.astype(dt), jacobi_c(g.data, w.astuple(), steps, dt))
+    assert rep.halo_exchanged_cells == 2 * (n_gpus - 1) * 16 * nx * ((steps - 1) // 16)
