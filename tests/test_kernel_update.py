@@ -119,3 +119,18 @@ def test_partial_cols_and_disjoint_regions_of_one_buffer():
     want[5:7, 1:7] = jacobi_numpy(src, ALL_02.astuple(), 1)[1:3, 1:7]
     j2d5pt_update(Window(buf, 1, 1, 6, 3), Window(buf, 1, 5, 6, 2), ALL_02, Rect(0, 0, 6, 2))
     assert np.array_equal(buf, want)
+
+
+@pytest.mark.gpu
+def test_power_of_two_scaling_and_locality():
+    g = fresh(11, 13, 8)
+    w = StencilWeights(0.3, 0.1, -0.25, 0.6, 0.25)
+    out = update_grid(g, w)
+    scaled = Grid2D(g.nx, g.ny, g.data * 2.0 ** 12)
+    assert np.array_equal(update_grid(scaled, w).interior, out.interior * 2.0 ** 12)
+    g = fresh(10, 9, 11)
+    h = Grid2D(g.nx, g.ny, g.data.copy())
+    h.interior[4, 6] += 0.5
+    diff = update_grid(g, ALL_02).interior != update_grid(h, ALL_02).interior
+    changed = {(int(x), int(y)) for y, x in zip(*np.nonzero(diff))}
+    assert 1 <= len(changed) and changed <= {(6, 4), (5, 4), (7, 4), (6, 3), (6, 5)}
