@@ -1405,6 +1405,15 @@ int solve_host_slabs(const T* in, T* out, int64_t nx, int64_t ny, int64_t pitch,
   // live on another GPU) whenever every slab runs the pipelined kernel; else
   // device-to-device copies after each epoch
   bool fused = (flags & DTB_FLAG_SLAB_COPY) == 0 && n_slabs > 1;
+  for (int g = 0; g + 1 < n_slabs && fused; ++g) {  // in-kernel stores need peer access
+    const int da = (dev0 + sl[g].dev) % ndev, db = (dev0 + sl[g + 1].dev) % ndev;
+    int ab = 1, ba = 1;
+    if (da != db) {
+      CUDA_TRY(cudaDeviceCanAccessPeer(&ab, da, db));
+      CUDA_TRY(cudaDeviceCanAccessPeer(&ba, db, da));
+    }
+    fused = ab && ba;
+  }
   if (fused) {
     DevInfo di;
     if (int rc = query_dev(di)) return rc;
