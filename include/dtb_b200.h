@@ -96,8 +96,9 @@ typedef struct dtb_plan_info {
  * change results. rep may be NULL. n_gpus >= 1: with n_gpus > 1 the library
  * splits the grid into n_gpus y-slabs over the visible devices (round-robin;
  * slabs share a device when fewer are visible), exchanging 16-row halos by
- * device-to-device copies (NVLink P2P) — bitwise equal to n_gpus = 1; not
- * combinable with a valid region. The call stays blocking. */
+ * device-to-device copies or in-kernel peer stores (NVLink P2P) — bitwise
+ * equal to n_gpus = 1, with or without a valid region. The call stays
+ * blocking. */
 int dtb_j2d5pt_f64(const double* in, double* out, int64_t nx, int64_t ny, int64_t pitch,
                    const double w[5], int64_t total_steps, int64_t t_depth,
                    const dtb_rect* valid, int ilp, int n_gpus, unsigned flags,

@@ -876,6 +876,7 @@ struct Arena {
 std::mutex g_mu;
 Arena g_scratch[16];
 Arena g_io[16];
+Arena g_stage[16];  // aligned staging copies of misaligned grid origins (solve_dev)
 
 int arena_get(Arena& a, size_t bytes, void** out) {
   if (a.n < bytes) {
@@ -1278,6 +1279,30 @@ int solve_dev(const T* d_in, T* d_out, int64_t nx, int64_t ny, int64_t pitch, co
   }
   const T* in_v = d_in + vy * pitch + vx;
   T* out_v = d_out + vy * pitch + vx;
+  if ((reinterpret_cast<uintptr_t>(in_v) | reinterpret_cast<uintptr_t>(out_v)) & 15) {
+    // the kernels move 16-byte chunks counted from the grid origin: solve a
+    // misaligned origin (an odd-column valid window, an offset view) in an
+    // aligned staging copy and copy the result back
+    const int64_t spitch = (vnx + 2 + 31) / 32 * 32;
+    const size_t sbytes = (size_t)(vny + 2) * spitch * sizeof(T), srow = (size_t)(vnx + 2) * sizeof(T);
+    int device;
+    CUDA_TRY(cudaGetDevice(&device));
+    void* sp = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      if (int rc2 = arena_get(g_stage[device & 15], 2 * sbytes, &sp)) return rc2;
+    }
+    T* s_in = reinterpret_cast<T*>(sp);
+    T* s_out = reinterpret_cast<T*>(reinterpret_cast<char*>(sp) + sbytes);
+    CUDA_TRY(cudaMemcpy2DAsync(s_in, spitch * sizeof(T), in_v, pitch * sizeof(T), srow, vny + 2,
+                               cudaMemcpyDeviceToDevice, st));
+    if (int rc2 = solve_dev<T>(s_in, s_out, vnx, vny, spitch, w, total_steps, t_depth, nullptr,
+                               flags, st, rep))
+      return rc2;
+    CUDA_TRY(cudaMemcpy2DAsync(out_v, pitch * sizeof(T), s_out, spitch * sizeof(T), srow, vny + 2,
+                               cudaMemcpyDeviceToDevice, st));
+    return DTB_OK;
+  }
   DevInfo dev;
   rc = query_dev(dev);
   if (rc) return rc;
@@ -1562,9 +1587,16 @@ int solve_host(const T* in, T* out, int64_t nx, int64_t ny, int64_t pitch, const
     if (int rc = validate(nx, ny, pitch, wd, total_steps,
                           (flags & DTB_FLAG_FORCE_DEPTH) ? 1 : t_depth, valid))
       return rc;
-    if (valid && !(valid->x0 == 0 && valid->y0 == 0 && valid->width == nx && valid->height == ny))
-      return fail(DTB_EINVAL, "a valid= region needs n_gpus = 1");
     g_err.clear();
+    if (valid && !(valid->x0 == 0 && valid->y0 == 0 && valid->width == nx && valid->height == ny)) {
+      // cells outside `valid` are frozen: copy them, then slab-solve the valid
+      // rectangle with its surrounding ring as ghost (engine.py:26-30, grid.py:199-222)
+      for (int64_t r = 0; r < ny + 2; ++r)
+        memcpy(out + r * pitch, in + r * pitch, (size_t)(nx + 2) * sizeof(T));
+      const int64_t off = valid->y0 * pitch + valid->x0;
+      return solve_host_slabs<T>(in + off, out + off, valid->width, valid->height, pitch, w,
+                                 total_steps, flags, n_gpus, rep);
+    }
     return solve_host_slabs<T>(in, out, nx, ny, pitch, w, total_steps, flags, n_gpus, rep);
   }
   double wd[5];

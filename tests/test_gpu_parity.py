@@ -326,3 +326,36 @@ def test_planner_experiment_knobs_stay_bitwise(env):
     assert len(lines) == 4 and all(l.endswith("True") for l in lines), r.stdout
     if key == "DTB_GROUPS":  # two tiles per CTA were really taken
         assert all(int(l.split()[5]) == 2 * int(l.split()[6]) for l in lines), r.stdout
+
+
+def test_misaligned_origins_valid_windows_and_offset_views():
+    """Odd-column valid windows (fp64) and x0 % 4 != 0 (fp32) put the solved
+    grid's origin off a 16-byte boundary; the device entry takes offset views
+    too. All must be bitwise equal to the oracle (the solve stages through an
+    aligned copy)."""
+    import torch
+    from paper_2306_03336_b200 import grid_extract, j2d5pt_device
+    w = MIXED
+    g = rgrid(300, 260, 3, ghost=0.125)
+    for v, dt in ((Rect(17, 9, 250, 231), np.float64), (Rect(1, 1, 7, 5), np.float64),
+                  (Rect(5, 3, 201, 100), np.float32), (Rect(2, 0, 298, 260), np.float32)):
+        for flags in (0, STREAM, _native.FLAG_FORCE_PIPE):
+            try:
+                out, _ = run_dtb_b200(g, w, 24, valid=v, dtype=dt, flags=flags)
+            except Exception as e:
+                assert "fit" in str(e) or "feasible" in str(e), e
+                continue
+            sub = grid_extract(g, v)
+            want = jacobi_c(sub.data, w.astuple(), 24, dt)
+            got = out.data[v.y0:v.y0 + v.height + 2, v.x0:v.x0 + v.width + 2]
+            assert same(got.astype(dt), want), (v, dt, flags)
+    # a device view starting one column into a buffer
+    nx, ny = 129, 77
+    base = torch.zeros((ny + 2, 1 + 160), dtype=torch.float64, device="cuda")
+    gg = rgrid(nx, ny, 9, ghost=0.5)
+    base[:, 1:nx + 3] = torch.from_numpy(gg.data).cuda()
+    src = base[:, 1:]
+    dst = torch.zeros_like(base)[:, 1:]
+    j2d5pt_device(src, dst, nx, ny, w, 10)
+    want = jacobi_c(gg.data, w.astuple(), 10)
+    assert np.array_equal(dst[:, :nx + 2].cpu().numpy().view(np.uint64), want.view(np.uint64))

@@ -83,3 +83,22 @@ def test_host_entry_fused_slab_halos_bitwise(n_gpus, nx, ny, steps, dt):
     assert np.array_equal(fused.data.view(np.uint64), copy.data.view(np.uint64))
     assert np.array_equal(fused.data.astype(dt), jacobi_c(g.data, w.astuple(), steps, dt))
     assert rep.halo_exchanged_cells == 2 * (n_gpus - 1) * 16 * nx * ((steps - 1) // 16)
+
+
+def test_host_entry_n_gpus_with_valid_region():
+    """A pruned (valid=) solve split over slabs equals the one-GPU pruned solve
+    and the oracle on the extracted region (engine.py:26-30)."""
+    from oracle import jacobi_c
+    from paper_2306_03336_b200 import Rect, StencilWeights, grid_extract, grid_new, run_dtb_b200
+    from paper_2306_03336_b200.prng import random_interior
+    g = grid_new(300, 260, random_interior(300, 260, 3), ghost=0.125)
+    w = StencilWeights(0.11, -0.2, 0.37, 0.5, -0.07)
+    v = Rect(17, 9, 250, 231)
+    one, _ = run_dtb_b200(g, w, 40, valid=v)
+    for n in (2, 3):
+        multi, rep = run_dtb_b200(g, w, 40, valid=v, n_gpus=n)
+        assert np.array_equal(multi.data.view(np.uint64), one.data.view(np.uint64))
+        assert rep.useful_compute_cells == 250 * 231 * 40
+    sub = grid_extract(g, v)
+    want = jacobi_c(sub.data, w.astuple(), 40)
+    assert np.array_equal(one.data[v.y0:v.y0 + v.height + 2, v.x0:v.x0 + v.width + 2], want)
