@@ -20,7 +20,8 @@ F = _native
 MODES = [0, F.FLAG_FORCE_STREAM, F.FLAG_FORCE_PIPE, F.FLAG_FORCE_RESIDENT, F.FLAG_FORCE_NAIVE]
 bad = skipped = 0
 for c in range(n_cases):
-    nx, ny = int(rng.integers(1, 900)), int(rng.integers(1, 900))
+    maxn = int(os.environ.get("FUZZ_MAXN", "900"))
+    nx, ny = int(rng.integers(1, maxn)), int(rng.integers(1, maxn))
     steps = int(rng.integers(1, 50))
     dt = np.float32 if rng.random() < 0.35 else np.float64
     g = grid_new(nx, ny, random_interior(nx, ny, c + seed), ghost=float(rng.choice([0.0, 0.375, -2.0])))
