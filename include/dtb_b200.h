@@ -110,7 +110,11 @@ int dtb_j2d5pt_f32(const float* in, float* out, int64_t nx, int64_t ny, int64_t 
 
 /* Device-pointer entry points on the current device; `stream` is a
  * cudaStream_t (NULL = legacy default). Asynchronous with respect to the host
- * except for plan/scratch setup; in and out must not alias. */
+ * except for plan/scratch setup; in and out must not alias. Solves share the
+ * device's scratch (halo exchange buffers, the streaming ping-pong buffer):
+ * solves queued on different streams must be ordered by the caller (one
+ * stream, or an event between them). Any origin alignment is accepted; a
+ * grid origin off a 16-byte boundary is solved in an aligned staging copy. */
 int dtb_j2d5pt_f64_dev(const double* d_in, double* d_out, int64_t nx, int64_t ny,
                        int64_t pitch, const double w[5], int64_t total_steps,
                        int64_t t_depth, const dtb_rect* valid, unsigned flags,
