@@ -280,6 +280,66 @@ __device__ __forceinline__ void warp_g2s_chunks(uint32_t sbase, const T* __restr
   }
 }
 
+// Thread-block cluster pair (DTB_CLUSTER): horizontally adjacent tiles
+// (tx, tx^1) run as one 2-CTA cluster, and the side strip a tile needs from
+// its partner is read straight out of the partner's shared memory (DSMEM)
+// instead of the L2 exchange buffer. Ordering: every thread arrives
+// (release) on the cluster barrier after its epoch's sweeps; the warp that
+// copies the partner strip waits (acquire) first, the others after their
+// tasks; the refresh closes with a full cluster barrier so the partner has
+// read my seam columns before my next sweep overwrites them.
+#ifndef DTB_CLUSTER
+#define DTB_CLUSTER 0
+#endif
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t dsmem_map(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+// remote loads carry no memory clobber so a batch of them is in flight at
+// once; the cluster barrier asm (volatile, clobbers memory) orders them
+__device__ __forceinline__ double dsmem_ld(uint32_t a, double) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float dsmem_ld(uint32_t a, float) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+// tile rect [r0, r1) x [c0, c1) <- partner tile (r, c + dc), one warp; each
+// lane issues 8 remote loads before its 8 local stores
+template <typename T, int K>
+__device__ __forceinline__ void warp_dsmem_strip(T* tile, uint32_t pbase, int r0, int r1,
+                                                 int c0, int c1, int dc, int lane) {
+  typedef Tile<T, K> L;
+  constexpr int B = 8;
+  const int w = c1 - c0, n = (r1 - r0) * w;
+  for (int i0 = lane; i0 < n; i0 += 32 * B) {
+    T v[B];
+    int d[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int i = i0 + 32 * u;
+      if (i < n) {
+        const int q = i / w, r = r0 + q, c = c0 + (i - q * w);
+        d[u] = L::at(r, c);
+        v[u] = dsmem_ld(pbase + (uint32_t)(L::at(r, c + dc) * (int)sizeof(T)), T());
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+      if (i0 + 32 * u < n) tile[d[u]] = v[u];
+  }
+}
+
 // Halo refresh, warp-specialised: the ring is cut into 16 tasks (N, S, the 4
 // corners, and the W and E side columns in 5 row slices each), each owned by
 // one neighbour; a warp polls that neighbour's epoch flag and streams the
@@ -291,7 +351,8 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
                                                      const int* flags, int epoch, int ntx, int nty,
                                                      int tx, int ty, int ry0, int oy0, int oy1,
                                                      int ry1, int rx0, int ox0, int ox1, int rx1,
-                                                     unsigned long long* mark = nullptr) {
+                                                     unsigned long long* mark = nullptr,
+                                                     int ptx = -1, uint32_t pbase = 0, int pdc = 0) {
   typedef Tile<T, K> L;
 #ifndef DTB_SIDE_PARTS
 #define DTB_SIDE_PARTS 1
@@ -302,6 +363,20 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
   const bool vec = ((gx0 % L::EPC) == 0) && ((pitch % L::EPC) == 0);
   const int side_rows = oy1 - oy0;
   int polled = -1;  // neighbour this warp last waited for
+  // Cluster phases per epoch: P1 (arrived by the caller after the sweeps)
+  // gates the partner-strip copy; P2 tells the partner its seam columns have
+  // been read. Warps without the copy pass P1 and arrive on P2 up front so
+  // the partner never waits for this CTA's global-memory refresh.
+  bool copy_warp = false;
+  if (DTB_CLUSTER && ptx >= 0) {
+    for (int k = warp; k < 6 + 2 * kSideParts; k += nw)
+      copy_warp |= k >= 6 && (((k - 6) < kSideParts) ? tx - 1 : tx + 1) == ptx;
+    if (!copy_warp) {
+      cluster_wait();
+      cluster_arrive();
+    }
+  }
+  bool waited = !copy_warp;
   for (int k = warp; k < 6 + 2 * kSideParts; k += nw) {
     int dx, dy, r0, r1, c0, c1;
     if (k < 6) {
@@ -325,6 +400,13 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
     }
     const int nxt = tx + dx, nyt = ty + dy;
     if (r1 <= r0 || c1 <= c0 || nxt < 0 || nxt >= ntx || nyt < 0 || nyt >= nty) continue;
+    if (DTB_CLUSTER && dy == 0 && nxt == ptx) {  // the cluster partner's strip: DSMEM
+      if (!waited) cluster_wait();
+      warp_dsmem_strip<T, K>(tile, pbase, r0, r1, c0, c1, pdc, lane);
+      if (!waited) cluster_arrive();
+      waited = true;
+      continue;
+    }
     const int nb = nyt * ntx + nxt;
     if (nb != polled) {
 #ifndef DTB_POLL
@@ -345,6 +427,10 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
       polled = nb;
     }
     warp_g2s_chunks<T, K>(sbase, g, pitch, gx0, gy0, r0, r1, c0, c1, vec, lane);
+  }
+  if (DTB_CLUSTER && !waited) {  // copy task was empty
+    cluster_wait();
+    cluster_arrive();
   }
   cp_async_wait_all();
 }
@@ -610,7 +696,8 @@ __global__ void __launch_bounds__(NW * 32 * G, 1)
 resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ xb0,
                 T* __restrict__ xb1, int* __restrict__ flags, int64_t pitch, int nx, int ny,
                 Weights<T> wt, int64_t total_steps, int h, int poison, int bs_on,
-                unsigned long long* __restrict__ trace, const __grid_constant__ Geometry geo) {
+                unsigned long long* __restrict__ trace, const __grid_constant__ Geometry geo,
+                int cl_on) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   constexpr int GT = G > 1 ? NW * 32 : 0;  // thread group = one tile
   const int group = G > 1 ? (int)(threadIdx.x / (NW * 32)) : 0;
@@ -649,6 +736,16 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
   // halo ring cells to refresh exclude the frozen ghost ring of the domain
   const int rx0 = hl ? 0 : 1, rx1 = hr ? Lw : Lw - 1, ry0 = ht ? 0 : 1, ry1 = hb ? Lh : Lh - 1;
 
+  // cluster partner (DTB_CLUSTER, launched as 2-CTA clusters along x): its tile
+  // index, its smem tile in the cluster window, and the column offset from my
+  // tile coordinates to its
+  int ptx = -1, pdc = 0;
+  uint32_t pbase = 0;
+  if (DTB_CLUSTER && cl_on) {
+    ptx = tx ^ 1;
+    pbase = dsmem_map((uint32_t)__cvta_generic_to_shared(tile), (uint32_t)(tx & 1) ^ 1u);
+    pdc = cx.z - geo.col[ptx].z;
+  }
   int64_t done = 0;
   int epoch = 0;
   unsigned long long t_comp = 0, t_pub = 0, t_wait = 0, t_ref = 0, t_pst = 0, t_pbar = 0, tc = 0;
@@ -741,15 +838,17 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
       // and immediately streams that region in (overlaps the 8 waits and loads)
       DTB_MARK(t_wait)
       unsigned long long t_poll = tc;
+      if (DTB_CLUSTER && cl_on) cluster_arrive();  // my sweeps are done (partner may read)
       refresh_by_direction<T, K, GT>(tile, xb, pitch, gx0, gy0, flags, epoch * flag_per_epoch,
                                  geo.ntx, geo.nty, tx, ty, ry0, oy0, oy1, ry1, rx0, ox0, ox1,
-                                 rx1, tracing ? &t_poll : nullptr);
+                                 rx1, tracing ? &t_poll : nullptr, ptx, pbase, pdc);
       if (tracing) {
         const unsigned long long now_ = clock64();
         t_wait += t_poll - tc;   // warp 0: until its first neighbour flag arrived
         t_pst += now_ - t_poll;  // warp 0: its loads
         tc = now_;
       }
+      if (DTB_CLUSTER && cl_on) cluster_wait();  // P2: the partner has read my seam columns
       gt_sync<GT>();
     } else {
     // 2. wait for the (up to 8) neighbours of this epoch
@@ -1031,11 +1130,46 @@ int launch_plan_kernels(const Plan& p, const Geometry& geo, const T* d_in, T* d_
     }
     int h = p.h;
     int pois = poison ? 1 : 0;
+    int cl_on = 0;
     void* args[] = {(void*)&d_in, (void*)&d_out, (void*)&xb0, (void*)&xb1, (void*)&flags,
                     (void*)&pitch, (void*)&nx, (void*)&ny, (void*)&wt, (void*)&steps,
-                    (void*)&h, (void*)&pois, (void*)&bs_on, (void*)&trace, (void*)&geo};
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(p.ctas), dim3(threads), args,
-                                         (size_t)smem_res, st));
+                    (void*)&h, (void*)&pois, (void*)&bs_on, (void*)&trace, (void*)&geo,
+                    (void*)&cl_on};
+    bool launched = false;
+    if (DTB_CLUSTER && G == 1 && geo.ntx % 2 == 0 && p.ctas % 2 == 0 && !getenv("DTB_CLUSTER_OFF")) {
+      // 2-CTA clusters along x, still a cooperative (co-resident) launch; if the
+      // device cannot co-schedule them, fall back to the plain launch below
+      cl_on = 1;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(p.ctas);
+      cfg.blockDim = dim3(threads);
+      cfg.dynamicSmemBytes = (size_t)smem_res;
+      cfg.stream = st;
+      cudaLaunchAttribute at[2];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      at[1].id = cudaLaunchAttributeCooperative;
+      at[1].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 2;
+      int nclusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)kern, &cfg) == cudaSuccess &&
+          nclusters * 2 >= p.ctas &&
+          cudaLaunchKernelExC(&cfg, (const void*)kern, args) == cudaSuccess) {
+        launched = true;
+      } else {
+        (void)cudaGetLastError();
+        cl_on = 0;
+      }
+      if (getenv("DTB_CLUSTER_VERBOSE"))
+        fprintf(stderr, "dtb: resident cluster launch %s (%d 2-CTA clusters co-resident, %d CTAs)\n",
+                launched ? "used" : "not possible", nclusters, p.ctas);
+    }
+    if (!launched)
+      CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(p.ctas), dim3(threads), args,
+                                           (size_t)smem_res, st));
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
     if (tracing) {
