@@ -291,8 +291,14 @@ __device__ __forceinline__ void warp_g2s_chunks(uint32_t sbase, const T* __restr
 #ifndef DTB_CLUSTER
 #define DTB_CLUSTER 0
 #endif
+#ifndef DTB_CLUSTER_RELAXED
+#define DTB_CLUSTER_RELAXED 0  // 1: relaxed arrives (timing probe only: no release ordering)
+#endif
 __device__ __forceinline__ void cluster_arrive() {
-  asm volatile("barrier.cluster.arrive.release;" ::: "memory");
+  if (DTB_CLUSTER_RELAXED)
+    asm volatile("barrier.cluster.arrive.relaxed;" ::: "memory");
+  else
+    asm volatile("barrier.cluster.arrive.release;" ::: "memory");
 }
 __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire;" ::: "memory");
@@ -402,7 +408,10 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
     if (r1 <= r0 || c1 <= c0 || nxt < 0 || nxt >= ntx || nyt < 0 || nyt >= nty) continue;
     if (DTB_CLUSTER && dy == 0 && nxt == ptx) {  // the cluster partner's strip: DSMEM
       if (!waited) cluster_wait();
-      warp_dsmem_strip<T, K>(tile, pbase, r0, r1, c0, c1, pdc, lane);
+#ifndef DTB_CLUSTER_NOCOPY
+#define DTB_CLUSTER_NOCOPY 0  // 1: timing probe, partner strip not copied (wrong results)
+#endif
+      if (!DTB_CLUSTER_NOCOPY) warp_dsmem_strip<T, K>(tile, pbase, r0, r1, c0, c1, pdc, lane);
       if (!waited) cluster_arrive();
       waited = true;
       continue;
