@@ -23,7 +23,10 @@
  *
  * Results are bitwise identical to the reference's jacobi_reference: every
  * cell update is ((((W*w + E*e) + S*s) + C*c) + N*n) with every product and
- * sum rounded separately (no FMA).
+ * sum rounded separately (no FMA). When w, e, s and n are bitwise equal (the
+ * reference's StencilWeights.diffusive) the kernels form each source cell's
+ * product x*w once and use it for all four neighbours — the same rounded
+ * numbers, 6 instead of 9 operations per cell update.
  */
 #ifndef DTB_B200_H
 #define DTB_B200_H
@@ -137,6 +140,12 @@ int64_t dtb_last_trace(int64_t* out, int64_t n);
 
 /* Kernel launches issued by the most recent solve on this thread. */
 int64_t dtb_last_launch_count(void);
+
+/* After a DTB_EINFEASIBLE: the smallest dynamic shared memory per CTA (bytes)
+ * a plan of the requested kind would need — the B200 counterpart of
+ * InfeasiblePlanError.min_required_bytes (planner.py:51-56, 222-228). 0 after
+ * any other outcome. */
+int64_t dtb_last_min_required_bytes(void);
 
 /* Device properties the planner uses (cudaDeviceGetAttribute). */
 int dtb_device_info(int32_t* sms, int64_t* smem_optin_per_block, int64_t* l2_bytes,

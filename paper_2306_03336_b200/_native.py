@@ -87,6 +87,7 @@ _SIGNATURES = {
     "dtb_plan": (c_int, [c_int64, c_int64, c_int32, c_int64, c_int64, c_uint,
                          POINTER(DtbPlanInfo)]),
     "dtb_last_launch_count": (c_int64, []),
+    "dtb_last_min_required_bytes": (c_int64, []),
     "dtb_last_trace": (c_int64, [POINTER(c_int64), c_int64]),
     "dtb_device_info": (c_int, [POINTER(c_int32), POINTER(c_int64), POINTER(c_int64),
                                 POINTER(c_int32), POINTER(c_int32)]),

@@ -2,6 +2,8 @@
 
 -fmad=false plus explicit __dmul_rn/__dadd_rn keeps every product and sum
 separately rounded, the reference's bitwise contract (kernel.py:3-11).
+The translation units (one per kernel family and element type, the host
+runtime, the planner) compile in parallel and link into one shared object.
 """
 
 from __future__ import annotations
@@ -9,41 +11,68 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libdtb_b200.so")
-SOURCES = ["dtb_kernels.cu", "dtb_plan.cpp"]
-HEADERS = ["dtb_core.cuh", "dtb_pipe.cuh", "dtb_plan.h",
-           os.path.join("..", "..", "include", "dtb_b200.h")]
+OBJ = os.path.join(HERE, "build")
+SOURCES = ["dtb_resident_f64.cu", "dtb_resident_f32.cu", "dtb_pipe_f64.cu", "dtb_pipe_f32.cu",
+           "dtb_stream.cu", "dtb_host.cu", "dtb_plan.cpp"]
+HEADER = os.path.join(HERE, "..", "include", "dtb_b200.h")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
 ]
+
+
+def _deps() -> list[str]:
+    return [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [HEADER, __file__]
 
 
 def _stale() -> bool:
     if not os.path.exists(OUT):
         return True
     t = os.path.getmtime(OUT)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [__file__]
-    deps += [os.path.join(CSRC, f) for f in os.listdir(CSRC)]  # any csrc file
-    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+    return any(os.path.getmtime(d) > t for d in _deps() if os.path.exists(d))
 
 
-def build_native(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build_native(force: bool = False, verbose: bool = False, defines: tuple[str, ...] = (),
+                 out: str | None = None) -> str:
+    """Compile every translation unit (in parallel) and link the library.
+    ``defines`` (e.g. ``("DTB_PIPE_PROBE=1",)``) and ``out`` build debug
+    variants beside the product library."""
+    target = out or OUT
+    if out is None and not defines and not force and not _stale():
         return OUT
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], "-o", OUT + ".tmp"]
+    tag = "_".join(d.replace("=", "") for d in defines) or "product"
+    objdir = os.path.join(OBJ, tag)
+    os.makedirs(objdir, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
+
+    def compile_one(src: str) -> str:
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+        cmd = [nvcc, *NVCC_FLAGS, *dflags, "-c", os.path.join(CSRC, src), "-o", obj]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs,
+           "-o", target + ".tmp"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build_native(force="--force" in sys.argv, verbose=True))
+    defs = tuple(a[2:] for a in sys.argv[1:] if a.startswith("-D"))
+    outp = next((a[6:] for a in sys.argv[1:] if a.startswith("--out=")), None)
+    print(build_native(force="--force" in sys.argv, verbose=True, defines=defs, out=outp))

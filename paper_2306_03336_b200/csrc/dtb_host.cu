@@ -1,0 +1,761 @@
+// dtb_host.cu — host runtime and the C ABI (include/dtb_b200.h).
+//
+// solve_dev: argument contract (engine.py:236-251), valid-region handling
+// (engine.py:26-30), the B200 plan (dtb_plan.cpp) and dispatch to a kernel
+// family (dtb_resident_*.cu, dtb_pipe_*.cu, dtb_stream.cu). solve_host_slabs:
+// n_gpus > 1 y-slabs with depth-16 halos. The C entry points
+// wrap these with host<->device copies.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "dtb_internal.h"
+
+namespace dtb {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+thread_local std::vector<int64_t> g_trace;
+thread_local unsigned g_flags = 0;
+thread_local const void* g_halo_mirror = nullptr;
+thread_local int64_t g_min_bytes = 0;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+namespace {
+struct Arena {
+  void* p = nullptr;
+  size_t n = 0;
+};
+std::mutex g_arena_mu;
+Arena g_arenas[kArenaCount][16];
+}  // namespace
+
+int arena_get(int role, int device, size_t bytes, void** out) {
+  std::lock_guard<std::mutex> lk(g_arena_mu);
+  Arena& a = g_arenas[role][device & 15];
+  if (a.n < bytes) {
+    if (a.p) cudaFree(a.p);
+    a.p = nullptr;
+    a.n = 0;
+    CUDA_TRY(cudaMalloc(&a.p, bytes));
+    a.n = bytes;
+  }
+  *out = a.p;
+  return DTB_OK;
+}
+
+// Per-call host work is on the critical path of short solves (C1: ~0.1 ms per
+// solve), so device attributes, kernel smem attributes and occupancy are
+// queried once per device / kernel and cached.
+static int query_dev_uncached(DevInfo& d, int dev) {
+  int v = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+  d.sms = v;
+  CUDA_TRY(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  d.smem_optin = v;
+  CUDA_TRY(cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev));
+  d.l2_bytes = v;
+  CUDA_TRY(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev));
+  d.smem_per_sm = v;
+  return DTB_OK;
+}
+
+int query_dev(DevInfo& d) {
+  static std::mutex mu;
+  static DevInfo cache[16];
+  static bool have[16] = {};
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  if (!have[dev & 15]) {
+    int rc = query_dev_uncached(cache[dev & 15], dev);
+    if (rc) return rc;
+    have[dev & 15] = true;
+  }
+  d = cache[dev & 15];
+  return DTB_OK;
+}
+
+int prepare_kernel(const void* kern, int device, int smem, int threads, int* per_sm) {
+  struct A {
+    const void* k;
+    int dev, smem;
+  };
+  struct O {
+    const void* k;
+    int dev, smem, threads, per_sm;
+  };
+  static std::mutex mu;
+  static std::vector<A> attrs;
+  static std::vector<O> occ;
+  std::lock_guard<std::mutex> lk(mu);
+  A* a = nullptr;
+  for (A& e : attrs)
+    if (e.k == kern && e.dev == device) a = &e;
+  if (!a || a->smem < smem) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    if (a) a->smem = smem;
+    else attrs.push_back({kern, device, smem});
+  }
+  if (!per_sm) return DTB_OK;
+  for (const O& e : occ)
+    if (e.k == kern && e.dev == device && e.smem == smem && e.threads == threads) {
+      *per_sm = e.per_sm;
+      return DTB_OK;
+    }
+  int n = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem));
+  occ.push_back({kern, device, smem, threads, n});
+  *per_sm = n;
+  return DTB_OK;
+}
+
+template <typename T>
+bool weights_isotropic(const T w[5]) {
+  uint64_t b[5] = {0, 0, 0, 0, 0};
+  for (int i = 0; i < 5; ++i) memcpy(&b[i], &w[i], sizeof(T));
+  return b[0] == b[1] && b[0] == b[2] && b[0] == b[4];
+}
+template bool weights_isotropic<double>(const double*);
+template bool weights_isotropic<float>(const float*);
+
+}  // namespace dtb
+
+// ===========================================================================
+namespace {
+
+using namespace dtb;
+
+int fill_geometry(const Plan& p, Geometry& g) {
+  if (p.sx.n > kMaxTiles || p.sy.n > kMaxTiles)
+    return fail(DTB_EINFEASIBLE, "plan needs %d x %d tiles (max %d per dimension)", p.sx.n,
+                p.sy.n, kMaxTiles);
+  memset(&g, 0, sizeof g);
+  g.ntx = p.sx.n;
+  g.nty = p.sy.n;
+  for (int i = 0; i < p.sx.n; ++i) g.col[i] = make_int4(p.sx.o0[i], p.sx.o1[i], p.sx.l0[i], p.sx.l1[i]);
+  for (int j = 0; j < p.sy.n; ++j) g.row[j] = make_int4(p.sy.o0[j], p.sy.o1[j], p.sy.l0[j], p.sy.l1[j]);
+  return DTB_OK;
+}
+
+int validate(int64_t nx, int64_t ny, int64_t pitch, const double w[5], int64_t total_steps,
+             int64_t t_depth, const dtb_rect* valid) {
+  if (nx < 1 || ny < 1) return fail(DTB_EINVAL, "grid dims must be at least 1x1, got %lldx%lld", (long long)nx, (long long)ny);
+  if (pitch < nx + 2) return fail(DTB_EINVAL, "pitch %lld smaller than nx+2 = %lld", (long long)pitch, (long long)(nx + 2));
+  for (int i = 0; i < 5; ++i)
+    if (!std::isfinite(w[i])) return fail(DTB_EINVAL, "non-finite stencil weight %c=%g", "wescn"[i], w[i]);
+  if (t_depth < 1) return fail(DTB_EINVAL, "t_depth must be at least 1, got %lld", (long long)t_depth);
+  if (total_steps < 1 || total_steps % t_depth)
+    return fail(DTB_EINVAL, "total_steps %lld is not a positive multiple of t_depth %lld",
+                (long long)total_steps, (long long)t_depth);
+  if (valid) {
+    if (valid->width < 0 || valid->height < 0)
+      return fail(DTB_EINVAL, "negative rect dims: %lldx%lld", (long long)valid->width, (long long)valid->height);
+    if (valid->width == 0 || valid->height == 0 || valid->x0 < 0 || valid->y0 < 0 ||
+        valid->x0 + valid->width > nx || valid->y0 + valid->height > ny)
+      return fail(DTB_EINVAL, "valid region (%lld, %lld, %lld, %lld) not within domain %lldx%lld",
+                  (long long)valid->x0, (long long)valid->y0, (long long)valid->width,
+                  (long long)valid->height, (long long)nx, (long long)ny);
+  }
+  return DTB_OK;
+}
+
+// The B200 schedule's traffic in the reference's cell units (metrics.py:39-66;
+// the ghost ring is never counted, metrics.py:3-6).
+void fill_report(const Plan& p, int64_t nx, int64_t ny, int64_t steps, int elem, dtb_report* rep) {
+  if (!rep) return;
+  memset(rep, 0, sizeof *rep);
+  rep->elem_bytes = elem;
+  rep->useful_compute_cells = nx * ny * steps;
+  if (p.mode == 2) {
+    rep->global_load_cells = nx * ny * steps;
+    rep->global_store_cells = nx * ny * steps;
+    return;
+  }
+  const int64_t passes = (steps + p.h - 1) / p.h;
+  int64_t load = 0, owned = nx * ny, halo_ring = 0;
+  for (int i = 0; i < p.sx.n; ++i)
+    for (int j = 0; j < p.sy.n; ++j) {
+      const int64_t dw = std::min<int64_t>(p.sx.l1[i], nx) - std::max(p.sx.l0[i], 0);
+      const int64_t dh = std::min<int64_t>(p.sy.l1[j], ny) - std::max(p.sy.l0[j], 0);
+      load += dw * dh;
+      halo_ring += dw * dh - (int64_t)(p.sx.o1[i] - p.sx.o0[i]) * (p.sy.o1[j] - p.sy.o0[j]);
+    }
+  if (p.mode == 0) {
+    rep->global_load_cells = load + (passes - 1) * halo_ring;
+    rep->global_store_cells = owned + (passes - 1) * halo_ring;
+    rep->halo_exchanged_cells = (passes - 1) * halo_ring;
+  } else {
+    rep->global_load_cells = passes * load;
+    rep->global_store_cells = passes * owned;
+    rep->halo_exchanged_cells = 0;
+  }
+  rep->redundant_compute_cells = p.computed_cells_per_step * steps - nx * ny * steps;
+  rep->scratchpad_peak_bytes = p.smem_bytes;
+}
+
+int plan_fail(const char* err, int64_t min_bytes) {
+  g_min_bytes = min_bytes;
+  return fail(DTB_EINFEASIBLE, "%s", err);
+}
+
+int force_mode(unsigned flags) {
+  return (flags & DTB_FLAG_FORCE_NAIVE) ? 2 : (flags & DTB_FLAG_FORCE_STREAM) ? 1
+         : (flags & DTB_FLAG_FORCE_PIPE) ? 3 : (flags & DTB_FLAG_FORCE_RESIDENT) ? 4 : 0;
+}
+
+template <typename T>
+int solve_dev(const T* d_in, T* d_out, int64_t nx, int64_t ny, int64_t pitch, const T w[5],
+              int64_t total_steps, int64_t t_depth, const dtb_rect* valid, unsigned flags,
+              cudaStream_t st, dtb_report* rep) {
+  double wd[5];
+  for (int i = 0; i < 5; ++i) wd[i] = (double)w[i];
+  int rc = validate(nx, ny, pitch, wd, total_steps,
+                    (flags & DTB_FLAG_FORCE_DEPTH) ? 1 : t_depth, valid);
+  if (rc) return rc;
+  if ((flags & DTB_FLAG_FORCE_DEPTH) && t_depth < 1)
+    return fail(DTB_EINVAL, "forced depth must be at least 1, got %lld", (long long)t_depth);
+  if (d_in == d_out) return fail(DTB_EINVAL, "input and output buffers alias");
+  g_launches = 0;
+  g_flags = flags;
+  g_trace.clear();
+  const size_t row_bytes = (size_t)(nx + 2) * sizeof(T);
+  // valid-region runs: frozen cells outside `valid` are carried by a copy of
+  // the (nx+2)-column grid (never the pitch padding beyond it), and the valid
+  // rectangle evolves as a standalone problem whose ghost ring is the
+  // surrounding frozen cells (engine.py:26-30, grid.py:199-222).
+  int64_t vx = 0, vy = 0, vnx = nx, vny = ny;
+  if (valid && !(valid->x0 == 0 && valid->y0 == 0 && valid->width == nx && valid->height == ny)) {
+    CUDA_TRY(cudaMemcpy2DAsync(d_out, pitch * sizeof(T), d_in, pitch * sizeof(T), row_bytes,
+                               ny + 2, cudaMemcpyDeviceToDevice, st));
+    vx = valid->x0; vy = valid->y0; vnx = valid->width; vny = valid->height;
+  }
+  const T* in_v = d_in + vy * pitch + vx;
+  T* out_v = d_out + vy * pitch + vx;
+  if ((reinterpret_cast<uintptr_t>(in_v) | reinterpret_cast<uintptr_t>(out_v)) & 15) {
+    // the kernels move 16-byte chunks counted from the grid origin: solve a
+    // misaligned origin (an odd-column valid window, an offset view) in an
+    // aligned staging copy and copy the result back
+    const int64_t spitch = (vnx + 2 + 31) / 32 * 32;
+    const size_t sbytes = (size_t)(vny + 2) * spitch * sizeof(T), srow = (size_t)(vnx + 2) * sizeof(T);
+    int device;
+    CUDA_TRY(cudaGetDevice(&device));
+    void* sp = nullptr;
+    if (int rc2 = arena_get(kArenaStage, device, 2 * sbytes, &sp)) return rc2;
+    T* s_in = reinterpret_cast<T*>(sp);
+    T* s_out = reinterpret_cast<T*>(reinterpret_cast<char*>(sp) + sbytes);
+    CUDA_TRY(cudaMemcpy2DAsync(s_in, spitch * sizeof(T), in_v, pitch * sizeof(T), srow, vny + 2,
+                               cudaMemcpyDeviceToDevice, st));
+    if (int rc2 = solve_dev<T>(s_in, s_out, vnx, vny, spitch, w, total_steps, t_depth, nullptr,
+                               flags, st, rep))
+      return rc2;
+    CUDA_TRY(cudaMemcpy2DAsync(out_v, pitch * sizeof(T), s_out, spitch * sizeof(T), srow, vny + 2,
+                               cudaMemcpyDeviceToDevice, st));
+    return DTB_OK;
+  }
+  DevInfo dev;
+  rc = query_dev(dev);
+  if (rc) return rc;
+  const int depth = (flags & DTB_FLAG_FORCE_DEPTH) ? (int)t_depth : 0;
+  Plan p;
+  char err[512];
+  int64_t min_bytes = 0;
+  if (!make_plan(vnx, vny, (int)sizeof(T), total_steps, dev, force_mode(flags), depth, p, err,
+                 sizeof err, &min_bytes))
+    return plan_fail(err, min_bytes);
+  const bool poison = (flags & DTB_FLAG_POISON) != 0;
+  if (g_halo_mirror && p.mode != 3)
+    return fail(DTB_EINVAL, "fused slab halos need the pipelined kernel (plan mode %d)", p.mode);
+  if (p.mode == 2) {
+    // naive: total_steps launches ping-ponging between out and scratch
+    const size_t grid_bytes = (size_t)(ny + 2) * pitch * sizeof(T);
+    T* tmp = nullptr;
+    if (total_steps > 1) {
+      void* s = nullptr;
+      int device;
+      CUDA_TRY(cudaGetDevice(&device));
+      if (int rc2 = arena_get(kArenaScratch, device, grid_bytes, &s)) return rc2;
+      tmp = reinterpret_cast<T*>(s);
+      if (valid)  // the frozen cells around the window, in the scratch parity too
+        CUDA_TRY(cudaMemcpy2DAsync(tmp, pitch * sizeof(T), d_in, pitch * sizeof(T), row_bytes,
+                                   ny + 2, cudaMemcpyDeviceToDevice, st));
+    }
+    T* tmp_v = tmp ? tmp + vy * pitch + vx : nullptr;
+    rc = launch_naive<T>(in_v, out_v, tmp_v, pitch, (int)vnx, (int)vny, w, total_steps, st);
+    if (rc) return rc;
+  } else {
+    Geometry geo;
+    rc = fill_geometry(p, geo);
+    if (rc) return rc;
+    if (p.mode == 0)
+      rc = launch_resident<T>(p, geo, in_v, out_v, pitch, (int)vnx, (int)vny, w, total_steps, poison, st);
+    else if (p.mode == 3)
+      rc = launch_pipe<T>(p, geo, in_v, out_v, pitch, (int)vnx, (int)vny, w, total_steps, st);
+    else
+      rc = launch_stream<T>(p, geo, in_v, out_v, pitch, (int)vnx, (int)vny, w, total_steps, poison, st);
+    if (rc) return rc;
+  }
+  fill_report(p, vnx, vny, total_steps, (int)sizeof(T), rep);
+  return DTB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// n_gpus > 1 from the host entry: y-slabs (the native twin of
+// slab.py). Slab g owns interior rows [y0, y1) and keeps a local padded grid
+// of those rows plus kSlabDepth halo rows towards each neighbour (the global
+// ghost row on the outer sides). Every epoch of s <= depth steps each slab
+// advances its local grid s steps with its outer rows frozen (the trapezoid
+// argument: owned rows stay exact), then receives depth rows from each
+// neighbour into its halo. Slabs go round-robin over the visible devices;
+// slabs sharing a device run in order on that device's stream, so no kernel
+// ever waits on another's. Bitwise equal to n_gpus = 1.
+// ---------------------------------------------------------------------------
+constexpr int kSlabDepth = 16;
+
+struct DevBuffers {
+  std::vector<std::pair<int, void*>> bufs;  // (device, pointer)
+  std::vector<std::pair<int, cudaStream_t>> streams;
+  std::vector<cudaEvent_t> events;
+  int home = -1;  // the caller's device, restored on exit
+  ~DevBuffers() {
+    for (auto& s : streams) { cudaSetDevice(s.first); cudaStreamSynchronize(s.second); }
+    for (auto& e : events) cudaEventDestroy(e);
+    for (auto& s : streams) { cudaSetDevice(s.first); cudaStreamDestroy(s.second); }
+    for (auto& b : bufs) { cudaSetDevice(b.first); cudaFree(b.second); }
+    if (home >= 0) cudaSetDevice(home);
+  }
+};
+
+// Peer access between two devices, enabled once. Usable only when enabling
+// succeeded or it was already enabled; any other failure (e.g. too many
+// peers) means in-kernel stores to the peer would fault, so callers fall
+// back to copies.
+bool peer_usable(int from, int to) {
+  if (from == to) return true;
+  static std::mutex mu;
+  static int state[16][16] = {};  // 0 unknown, 1 usable, 2 not usable
+  std::lock_guard<std::mutex> lk(mu);
+  int& s = state[from & 15][to & 15];
+  if (s == 0) {
+    int can = 0;
+    if (cudaDeviceCanAccessPeer(&can, from, to) != cudaSuccess) can = 0;
+    s = 2;
+    if (can) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(from);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+      if (e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled) s = 1;
+      cudaGetLastError();  // clear a non-sticky enable error
+      cudaSetDevice(cur);
+    }
+  }
+  return s == 1;
+}
+
+template <typename T>
+int solve_host_slabs(const T* in, T* out, int64_t nx, int64_t ny, int64_t pitch, const T w[5],
+                     int64_t total_steps, unsigned flags, int n_slabs, dtb_report* rep) {
+  if (ny < n_slabs)
+    return fail(DTB_EINVAL, "%lld rows cannot be split over %d GPUs", (long long)ny, n_slabs);
+  int ndev = 0, dev0 = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  CUDA_TRY(cudaGetDevice(&dev0));
+  if (ndev < 1) return fail(DTB_ECUDA, "no CUDA device");
+  const int64_t base = ny / n_slabs, rem = ny % n_slabs;
+  const int depth = (int)std::min<int64_t>(kSlabDepth, base);
+  struct Slab { int dev; int64_t y0, own, ht, hb, lny, row0; T* a; T* b; };
+  std::vector<Slab> sl(n_slabs);
+  const int64_t dpitch = (nx + 2 + 31) / 32 * 32;
+  const size_t hrow = (size_t)(nx + 2) * sizeof(T), drow = (size_t)dpitch * sizeof(T);
+  DevBuffers res;
+  res.home = dev0;
+  std::vector<cudaStream_t> dstream(std::min(ndev, n_slabs));
+  auto devof = [&](int d) { return (dev0 + d) % ndev; };
+  for (int d = 0; d < (int)dstream.size(); ++d) {
+    CUDA_TRY(cudaSetDevice(devof(d)));
+    CUDA_TRY(cudaStreamCreateWithFlags(&dstream[d], cudaStreamNonBlocking));
+    res.streams.push_back({devof(d), dstream[d]});
+  }
+  int64_t y = 0;
+  for (int g = 0; g < n_slabs; ++g) {
+    Slab& s = sl[g];
+    s.dev = g % (int)dstream.size();
+    s.y0 = y;
+    s.own = base + (g < rem ? 1 : 0);
+    y += s.own;
+    s.ht = g > 0 ? depth : 1;
+    s.hb = g + 1 < n_slabs ? depth : 1;
+    s.lny = s.own + s.ht + s.hb - 2;
+    s.row0 = s.y0 + 1 - s.ht;  // padded global row of local row 0
+    const size_t bytes = (size_t)(s.lny + 2) * drow;
+    CUDA_TRY(cudaSetDevice(devof(s.dev)));
+    void* p = nullptr;
+    CUDA_TRY(cudaMalloc(&p, 2 * bytes));
+    res.bufs.push_back({devof(s.dev), p});
+    s.a = reinterpret_cast<T*>(p);
+    s.b = reinterpret_cast<T*>(reinterpret_cast<char*>(p) + bytes);
+    CUDA_TRY(cudaMemcpy2DAsync(s.a, drow, in + s.row0 * pitch, pitch * sizeof(T), hrow,
+                               s.lny + 2, cudaMemcpyHostToDevice, dstream[s.dev]));
+  }
+  // exchange mode: fused (the pipe kernel's final pass of each epoch stores
+  // the neighbours' halo rows straight into their next input, P2P when they
+  // live on another GPU) whenever every slab runs the pipelined kernel and
+  // every neighbour pair has usable peer access; else device-to-device
+  // copies after each epoch
+  bool fused = (flags & DTB_FLAG_SLAB_COPY) == 0 && n_slabs > 1;
+  for (int g = 0; g + 1 < n_slabs && fused; ++g) {
+    const int da = devof(sl[g].dev), db = devof(sl[g + 1].dev);
+    fused = peer_usable(da, db) && peer_usable(db, da);
+  }
+  if (n_slabs > 1 && !fused) {  // best effort: direct NVLink copies
+    for (int g = 0; g + 1 < n_slabs; ++g) {
+      const int da = devof(sl[g].dev), db = devof(sl[g + 1].dev);
+      peer_usable(da, db);
+      peer_usable(db, da);
+    }
+  }
+  CUDA_TRY(cudaSetDevice(dev0));
+  if (fused) {
+    DevInfo di;
+    if (int rc = query_dev(di)) return rc;
+    const int force = (flags & DTB_FLAG_SLAB_FUSED) ? 3 : 0;
+    for (int g = 0; g < n_slabs && fused; ++g) {
+      Plan p;
+      char err[256];
+      fused = make_plan(nx, sl[g].lny, (int)sizeof(T), depth, di, force, 0, p, err, sizeof err,
+                        nullptr) &&
+              p.mode == 3;
+    }
+  }
+  if ((flags & DTB_FLAG_SLAB_FUSED) && !fused)
+    return fail(DTB_EINFEASIBLE, "fused slab halos need the pipelined kernel and peer access on every slab");
+  std::vector<cudaEvent_t> solved(2 * n_slabs), copied(n_slabs);  // solved: epoch parity
+  for (int g = 0; g < n_slabs; ++g) {
+    CUDA_TRY(cudaSetDevice(devof(sl[g].dev)));
+    for (int k = 0; k < 2; ++k) {
+      CUDA_TRY(cudaEventCreateWithFlags(&solved[k * n_slabs + g], cudaEventDisableTiming));
+      res.events.push_back(solved[k * n_slabs + g]);
+    }
+    CUDA_TRY(cudaEventCreateWithFlags(&copied[g], cudaEventDisableTiming));
+    res.events.push_back(copied[g]);
+  }
+  struct MirrorScope {  // g_halo_mirror for exactly one slab solve
+    explicit MirrorScope(const void* m) { g_halo_mirror = m; }
+    ~MirrorScope() { g_halo_mirror = nullptr; }
+  };
+  dtb_report acc;
+  memset(&acc, 0, sizeof acc);
+  int64_t launches = 0, done = 0;
+  int epoch = 0;
+  const unsigned lflags = (flags & ~(unsigned)(DTB_FLAG_FORCE_DEPTH | DTB_FLAG_SLAB_COPY |
+                                                DTB_FLAG_SLAB_FUSED)) |
+                          (fused ? (unsigned)DTB_FLAG_FORCE_PIPE : 0u);
+  std::vector<T*> next(n_slabs);
+  while (done < total_steps) {
+    const int64_t s_ep = std::min<int64_t>(depth, total_steps - done);
+    const int cur = epoch & 1, prev = cur ^ 1;
+    for (int g = 0; g < n_slabs; ++g) next[g] = sl[g].b;  // this epoch's outputs
+    for (int g = 0; g < n_slabs; ++g) {
+      Slab& s = sl[g];
+      cudaStream_t st = dstream[s.dev];
+      CUDA_TRY(cudaSetDevice(devof(s.dev)));
+      if (epoch > 0) {
+        if (fused) {
+          // our halo rows in s.a came from the neighbours' previous epoch, and the
+          // buffers we are about to write into were read by that epoch
+          if (g > 0) CUDA_TRY(cudaStreamWaitEvent(st, solved[prev * n_slabs + g - 1], 0));
+          if (g + 1 < n_slabs) CUDA_TRY(cudaStreamWaitEvent(st, solved[prev * n_slabs + g + 1], 0));
+        } else {
+          // the neighbours' last reads of our previous result buffer (their halo copies) are done
+          if (g > 0) CUDA_TRY(cudaStreamWaitEvent(st, copied[g - 1], 0));
+          if (g + 1 < n_slabs) CUDA_TRY(cudaStreamWaitEvent(st, copied[g + 1], 0));
+        }
+      }
+      HaloMirror<T> m;
+      memset(&m, 0, sizeof m);
+      m.sw0 = g == 0 ? 0 : s.ht;
+      m.sw1 = g + 1 == n_slabs ? s.lny + 2 : s.ht + s.own;
+      if (g > 0) {  // our first owned rows -> the upper slab's bottom halo
+        const Slab& u = sl[g - 1];
+        m.peer[0] = next[g - 1];
+        m.r0[0] = s.ht;
+        m.r1[0] = s.ht + depth;
+        m.p0[0] = u.ht + u.own;
+      }
+      if (g + 1 < n_slabs) {  // our last owned rows -> the lower slab's top halo
+        m.peer[1] = next[g + 1];
+        m.r0[1] = s.ht + s.own - depth;
+        m.r1[1] = s.ht + s.own;
+        m.p0[1] = 0;
+      }
+      dtb_report r;
+      {
+        MirrorScope scope(fused ? &m : nullptr);
+        if (int rc = solve_dev<T>(s.a, s.b, nx, s.lny, dpitch, w, s_ep, 1, nullptr, lflags, st, &r))
+          return rc;
+      }
+      launches += g_launches;
+      acc.global_load_cells += r.global_load_cells;
+      acc.global_store_cells += r.global_store_cells;
+      acc.redundant_compute_cells += r.redundant_compute_cells + r.useful_compute_cells;
+      acc.scratchpad_peak_bytes = std::max(acc.scratchpad_peak_bytes, r.scratchpad_peak_bytes);
+      std::swap(s.a, s.b);
+      CUDA_TRY(cudaEventRecord(solved[cur * n_slabs + g], st));
+    }
+    done += s_ep;
+    ++epoch;
+    if (done >= total_steps) break;
+    if (fused) {
+      acc.halo_exchanged_cells += 2 * (int64_t)(n_slabs - 1) * depth * nx;
+      continue;
+    }
+    for (int g = 0; g < n_slabs; ++g) {  // halo rows from each neighbour's owned edge rows
+      Slab& s = sl[g];
+      cudaStream_t st = dstream[s.dev];
+      CUDA_TRY(cudaSetDevice(devof(s.dev)));
+      if (g > 0) {
+        const Slab& u = sl[g - 1];
+        CUDA_TRY(cudaStreamWaitEvent(st, solved[cur * n_slabs + g - 1], 0));
+        CUDA_TRY(cudaMemcpy2DAsync(s.a, drow, u.a + (u.ht + u.own - depth) * dpitch, drow, hrow,
+                                   depth, cudaMemcpyDefault, st));
+        acc.halo_exchanged_cells += depth * nx;
+      }
+      if (g + 1 < n_slabs) {
+        const Slab& d = sl[g + 1];
+        CUDA_TRY(cudaStreamWaitEvent(st, solved[cur * n_slabs + g + 1], 0));
+        CUDA_TRY(cudaMemcpy2DAsync(s.a + (s.ht + s.own) * dpitch, drow, d.a + d.ht * dpitch, drow,
+                                   hrow, depth, cudaMemcpyDefault, st));
+        acc.halo_exchanged_cells += depth * nx;
+      }
+      CUDA_TRY(cudaEventRecord(copied[g], st));
+    }
+  }
+  for (int g = 0; g < n_slabs; ++g) {  // owned rows (and the global ghost rows) back
+    const Slab& s = sl[g];
+    CUDA_TRY(cudaSetDevice(devof(s.dev)));
+    const int64_t r0 = g == 0 ? 0 : s.ht, r1 = s.ht + s.own + (g + 1 == n_slabs ? 1 : 0);
+    CUDA_TRY(cudaMemcpy2DAsync(out + (s.row0 + r0) * pitch, pitch * sizeof(T), s.a + r0 * dpitch,
+                               drow, hrow, r1 - r0, cudaMemcpyDeviceToHost, dstream[s.dev]));
+  }
+  for (int d = 0; d < (int)dstream.size(); ++d) {
+    CUDA_TRY(cudaSetDevice(devof(d)));
+    CUDA_TRY(cudaStreamSynchronize(dstream[d]));
+  }
+  g_launches = launches;
+  if (rep) {
+    *rep = acc;
+    rep->elem_bytes = (int64_t)sizeof(T);
+    rep->useful_compute_cells = nx * ny * total_steps;
+    rep->redundant_compute_cells -= rep->useful_compute_cells;
+  }
+  return DTB_OK;
+}
+
+template <typename T>
+int solve_host(const T* in, T* out, int64_t nx, int64_t ny, int64_t pitch, const T w[5],
+               int64_t total_steps, int64_t t_depth, const dtb_rect* valid, int ilp, int n_gpus,
+               unsigned flags, dtb_report* rep) {
+  if (!in || !out) return fail(DTB_EINVAL, "null buffer");
+  if (ilp < 1) return fail(DTB_EINVAL, "ilp must be at least 1, got %d", ilp);
+  if (n_gpus < 1) return fail(DTB_EINVAL, "n_gpus must be at least 1, got %d", n_gpus);
+  double wd[5];
+  for (int i = 0; i < 5; ++i) wd[i] = (double)w[i];
+  int rc = validate(nx, ny, pitch, wd, total_steps,
+                    (flags & DTB_FLAG_FORCE_DEPTH) ? 1 : t_depth, valid);
+  if (rc) return rc;
+  if (n_gpus > 1) {
+    if (valid && !(valid->x0 == 0 && valid->y0 == 0 && valid->width == nx && valid->height == ny)) {
+      // cells outside `valid` are frozen: copy them, then slab-solve the valid
+      // rectangle with its surrounding ring as ghost (engine.py:26-30, grid.py:199-222)
+      for (int64_t r = 0; r < ny + 2; ++r)
+        memcpy(out + r * pitch, in + r * pitch, (size_t)(nx + 2) * sizeof(T));
+      const int64_t off = valid->y0 * pitch + valid->x0;
+      return solve_host_slabs<T>(in + off, out + off, valid->width, valid->height, pitch, w,
+                                 total_steps, flags, n_gpus, rep);
+    }
+    return solve_host_slabs<T>(in, out, nx, ny, pitch, w, total_steps, flags, n_gpus, rep);
+  }
+  int device;
+  CUDA_TRY(cudaGetDevice(&device));
+  // device copy with a 128-byte-multiple pitch: 16-byte aligned tile copies
+  const int64_t dpitch = (nx + 2 + 31) / 32 * 32;
+  const size_t bytes = (size_t)(ny + 2) * dpitch * sizeof(T);
+  void* io = nullptr;
+  if ((rc = arena_get(kArenaIo, device, 2 * bytes, &io))) return rc;
+  T* d_in = reinterpret_cast<T*>(io);
+  T* d_out = reinterpret_cast<T*>(reinterpret_cast<char*>(io) + bytes);
+  cudaStream_t st = 0;
+  const size_t row = (size_t)(nx + 2) * sizeof(T);
+  CUDA_TRY(cudaMemcpy2DAsync(d_in, dpitch * sizeof(T), in, pitch * sizeof(T), row, ny + 2,
+                             cudaMemcpyHostToDevice, st));
+  rc = solve_dev<T>(d_in, d_out, nx, ny, dpitch, w, total_steps, t_depth, valid, flags, st, rep);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpy2DAsync(out, pitch * sizeof(T), d_out, dpitch * sizeof(T), row, ny + 2,
+                             cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return DTB_OK;
+}
+
+void reset_call_state() {
+  g_err.clear();
+  g_min_bytes = 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dtb_j2d5pt_f64(const double* in, double* out, int64_t nx, int64_t ny, int64_t pitch,
+                   const double w[5], int64_t total_steps, int64_t t_depth,
+                   const dtb_rect* valid, int ilp, int n_gpus, unsigned flags,
+                   dtb_report* rep) {
+  reset_call_state();
+  return solve_host<double>(in, out, nx, ny, pitch, w, total_steps, t_depth, valid, ilp, n_gpus,
+                            flags, rep);
+}
+
+int dtb_j2d5pt_f32(const float* in, float* out, int64_t nx, int64_t ny, int64_t pitch,
+                   const float w[5], int64_t total_steps, int64_t t_depth,
+                   const dtb_rect* valid, int ilp, int n_gpus, unsigned flags,
+                   dtb_report* rep) {
+  reset_call_state();
+  return solve_host<float>(in, out, nx, ny, pitch, w, total_steps, t_depth, valid, ilp, n_gpus,
+                           flags, rep);
+}
+
+int dtb_j2d5pt_f64_dev(const double* d_in, double* d_out, int64_t nx, int64_t ny,
+                       int64_t pitch, const double w[5], int64_t total_steps,
+                       int64_t t_depth, const dtb_rect* valid, unsigned flags,
+                       void* stream, dtb_report* rep) {
+  reset_call_state();
+  return solve_dev<double>(d_in, d_out, nx, ny, pitch, w, total_steps, t_depth, valid, flags,
+                           (cudaStream_t)stream, rep);
+}
+
+int dtb_j2d5pt_f32_dev(const float* d_in, float* d_out, int64_t nx, int64_t ny,
+                       int64_t pitch, const float w[5], int64_t total_steps,
+                       int64_t t_depth, const dtb_rect* valid, unsigned flags,
+                       void* stream, dtb_report* rep) {
+  reset_call_state();
+  return solve_dev<float>(d_in, d_out, nx, ny, pitch, w, total_steps, t_depth, valid, flags,
+                          (cudaStream_t)stream, rep);
+}
+
+int dtb_plan(int64_t nx, int64_t ny, int32_t elem_bytes, int64_t total_steps, int64_t t_depth,
+             unsigned flags, dtb_plan_info* out) {
+  reset_call_state();
+  if (!out) return fail(DTB_EINVAL, "null plan output");
+  if (elem_bytes != 4 && elem_bytes != 8) return fail(DTB_EINVAL, "elem_bytes must be 4 or 8, got %d", elem_bytes);
+  DevInfo dev;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0) {
+    int rc = query_dev(dev);
+    if (rc) return rc;
+  } else {
+    cudaGetLastError();  // no GPU: plan for the B200 defaults (148 SMs, 227 KB)
+  }
+  const int depth = (flags & DTB_FLAG_FORCE_DEPTH) ? (int)t_depth : 0;
+  Plan p;
+  char err[512];
+  int64_t min_bytes = 0;
+  if (!make_plan(nx, ny, elem_bytes, total_steps, dev, force_mode(flags), depth, p, err,
+                 sizeof err, &min_bytes))
+    return plan_fail(err, min_bytes);
+  memset(out, 0, sizeof *out);
+  out->mode = p.mode;
+  out->elem_bytes = elem_bytes;
+  out->lane_elems = p.K;
+  out->warps = p.warps;
+  out->halo = p.h;
+  out->tiles_x = p.sx.n;
+  out->tiles_y = p.sy.n;
+  out->ctas = p.ctas;
+  out->ctas_per_sm = p.ctas_per_sm;
+  out->dyn = p.dyn() ? 1 : 0;
+  out->smem_bytes = p.smem_bytes;
+  for (int i = 0; i < p.sx.n; ++i) {
+    out->tile_w = std::max<int64_t>(out->tile_w, p.sx.o1[i] - p.sx.o0[i]);
+    out->load_w = std::max<int64_t>(out->load_w, p.sx.l1[i] - p.sx.l0[i]);
+  }
+  for (int j = 0; j < p.sy.n; ++j) {
+    out->tile_h = std::max<int64_t>(out->tile_h, p.sy.o1[j] - p.sy.o0[j]);
+    out->load_h = std::max<int64_t>(out->load_h, p.sy.l1[j] - p.sy.l0[j]);
+  }
+  out->computed_cells_per_step = p.computed_cells_per_step;
+  out->est_cells_per_clk = p.cells_per_clk;
+  return DTB_OK;
+}
+
+int64_t dtb_last_launch_count(void) { return g_launches; }
+
+int64_t dtb_last_min_required_bytes(void) { return g_min_bytes; }
+
+int64_t dtb_last_trace(int64_t* out, int64_t n) {
+  const int64_t m = std::min<int64_t>(n, (int64_t)g_trace.size());
+  for (int64_t i = 0; i < m && out; ++i) out[i] = g_trace[(size_t)i];
+  return (int64_t)g_trace.size() / 8;
+}
+
+int dtb_device_info(int32_t* sms, int64_t* smem_optin_per_block, int64_t* l2_bytes,
+                    int32_t* cc_major, int32_t* cc_minor) {
+  reset_call_state();
+  DevInfo d;
+  int rc = query_dev(d);
+  if (rc) return rc;
+  int dev = 0, maj = 0, mnr = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&maj, cudaDevAttrComputeCapabilityMajor, dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&mnr, cudaDevAttrComputeCapabilityMinor, dev));
+  if (sms) *sms = d.sms;
+  if (smem_optin_per_block) *smem_optin_per_block = d.smem_optin;
+  if (l2_bytes) *l2_bytes = d.l2_bytes;
+  if (cc_major) *cc_major = maj;
+  if (cc_minor) *cc_minor = mnr;
+  return DTB_OK;
+}
+
+int dtb_fill_random_f64(double* d_out, int64_t nx, int64_t ny, int64_t pitch, uint64_t seed,
+                        double ghost, void* stream) {
+  reset_call_state();
+  if (nx < 1 || ny < 1 || pitch < nx + 2) return fail(DTB_EINVAL, "bad fill dims");
+  return launch_fill<double>(d_out, pitch, (int)nx, (int)ny, seed, ghost, 0, ny + 2,
+                             (cudaStream_t)stream);
+}
+
+int dtb_fill_random_f32(float* d_out, int64_t nx, int64_t ny, int64_t pitch, uint64_t seed,
+                        double ghost, void* stream) {
+  reset_call_state();
+  if (nx < 1 || ny < 1 || pitch < nx + 2) return fail(DTB_EINVAL, "bad fill dims");
+  return launch_fill<float>(d_out, pitch, (int)nx, (int)ny, seed, ghost, 0, ny + 2,
+                            (cudaStream_t)stream);
+}
+
+int dtb_fill_random_rows_f64(double* d_out, int64_t nx, int64_t ny, int64_t pitch, uint64_t seed,
+                             double ghost, int64_t row0, int64_t nrows, void* stream) {
+  reset_call_state();
+  if (nx < 1 || ny < 1 || pitch < nx + 2 || row0 < 0 || nrows < 0 || row0 + nrows > ny + 2)
+    return fail(DTB_EINVAL, "bad fill rows");
+  return launch_fill<double>(d_out, pitch, (int)nx, (int)ny, seed, ghost, row0, nrows,
+                             (cudaStream_t)stream);
+}
+
+const char* dtb_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

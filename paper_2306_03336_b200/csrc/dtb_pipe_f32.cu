@@ -1,0 +1,5 @@
+// fp32 instantiation of the pipelined streaming kernel family (dtb_pipe.cuh).
+#include "dtb_pipe.cuh"
+
+template int dtb::launch_pipe<float>(const Plan&, const Geometry&, const float*, float*,
+                                     int64_t, int, int, const float*, int64_t, cudaStream_t);

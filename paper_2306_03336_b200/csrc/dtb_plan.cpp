@@ -2,9 +2,6 @@
 #include "dtb_plan.h"
 
 #include <algorithm>
-#ifndef DTB_PIPE_STAGES
-#define DTB_PIPE_STAGES 4  // pipeline stage warps (2 steps each): h = 2 * stages
-#endif
 #include <mutex>
 #include <string>
 #include <cmath>
@@ -82,33 +79,15 @@ namespace {
 
 struct Shape { int K; int warps; };
 
-constexpr int kPipeRing0Rows = 16;  // dtb_pipe.cuh kRing0Rows
-constexpr int kPipeRingRows = 8;    // dtb_pipe.cuh kRingRows
+// dtb_pipe.cuh kPipeWarps / kPipeStages / PipeCfg
+constexpr int kPlanPipeWarps = 16, kPlanPipeStages = 4;
 
-// kernel shapes compiled into libdtb_b200.so (dtb_kernels.cu dispatch)
+// kernel shapes compiled into libdtb_b200.so (dtb_resident.cuh / dtb_stream.cu):
+// 32 B of row state per lane (fp64 K=4, fp32 K=8: one 1 KB smem row per
+// warp-row), 8 warps
 std::vector<Shape> shapes_for(int elem) {
-  std::vector<Shape> v;
-  // 32 B of row state per lane, 8 warps (<= 255 registers: the 4-deep t and
-  // t+1 windows, the pre-read halo rows and the output row stay in registers;
-  // 16 warps (<= 128 registers) and 64 B per lane both spill)
-  if (elem == 8) v = {{4, 8}};
-  else v = {{8, 8}};
-#ifdef DTB_W12
-  if (elem == 8) v.push_back({4, 12});
-#endif
-#ifdef DTB_W4
-  if (elem == 8) v.push_back({4, 4});
-#endif
-  // DTB_SHAPE=K,W pins one shape (experiments)
-  if (const char* e = getenv("DTB_SHAPE")) {
-    int k = 0, w = 0;
-    if (sscanf(e, "%d,%d", &k, &w) == 2) {
-      std::vector<Shape> f;
-      for (auto& s : v) if (s.K == k && s.warps == w) f.push_back(s);
-      if (!f.empty()) return f;
-    }
-  }
-  return v;
+  if (elem == 8) return {{4, 8}};
+  return {{8, 8}};
 }
 
 std::vector<int> depths_for(int depth) {
@@ -123,18 +102,10 @@ double lanes_per_clk(int elem) { return elem == 8 ? 64.0 : 128.0; }
 // clock), so the non-FP instructions per row cost throughput there.
 double fp_efficiency(int elem) { return elem == 8 ? 0.92 : 0.80; }
 
-// Band heights exactly as the kernel splits them (dtb_core.cuh band_rows4 /
-// band_rows): two-step sweeps use whole 4-row quads per band (static fast
-// path), the last band takes the remainder (general path).
-static void band_heights(int rows, int nb, bool quads, std::vector<int>& hts) {
+// Band heights exactly as the kernel splits them (dtb_core.cuh band_rows).
+static void band_heights(int rows, int nb, std::vector<int>& hts) {
   hts.assign(nb, 0);
-  const int q = rows / 4;
-  if (!quads || q < nb) {
-    for (int b = 0; b < nb; ++b) hts[b] = rows / nb + (b < rows % nb ? 1 : 0);
-    return;
-  }
-  for (int b = 0; b < nb; ++b) hts[b] = 4 * (q / nb + (b < q % nb ? 1 : 0));
-  hts[nb - 1] += rows - 4 * q;
+  for (int b = 0; b < nb; ++b) hts[b] = rows / nb + (b < rows % nb ? 1 : 0);
 }
 
 // SM cycles for one CTA to advance a (Lw x Lh) tile by `steps` steps. Warp w
@@ -150,19 +121,16 @@ double tile_cycles(int elem, int K, int warps, int Lh, int steps) {
   std::vector<int> hts;
   if (s >= 2 && rows >= 2) {
     const int nb = std::max(1, std::min(warps, rows / 2));
-    band_heights(rows, nb, true, hts);
+    band_heights(rows, nb, hts);
     double smsp[4] = {0, 0, 0, 0};
-    for (int b = 0; b < nb; ++b) {
-      const bool fast = hts[b] % 4 == 0 && hts[b] >= 4;
-      smsp[b % 4] += (2.0 * hts[b] + 2.0) * row_cost * (fast ? 1.0 : 1.25);
-    }
+    for (int b = 0; b < nb; ++b) smsp[b % 4] += (2.0 * hts[b] + 2.0) * row_cost;
     const double sweep = *std::max_element(smsp, smsp + 4) + 400.0;  // + barriers, fill
     cyc += (s / 2) * sweep;
     s %= 2;
   }
   if (s) {
     const int nb = std::max(1, std::min(warps, rows));
-    band_heights(rows, nb, false, hts);
+    band_heights(rows, nb, hts);
     double smsp[4] = {0, 0, 0, 0};
     for (int b = 0; b < nb; ++b) smsp[b % 4] += hts[b] * row_cost * 1.25;
     cyc += s * (*std::max_element(smsp, smsp + 4) + 300.0);
@@ -220,58 +188,6 @@ bool plan_resident(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInf
             best.ctas = ntx * nty;
             best.ctas_per_sm = 1;
             best.smem_bytes = (int64_t)sy.max_load * row_bytes;
-            best.cycles_per_step = per_step;
-            best.cells_per_clk = cpc;
-          }
-        }
-        if (sx.max_load < Lw_max / 2 && ntx > ntx_min) break;
-      }
-    }
-  }
-  // two tiles per CTA (4-warp groups, vertically adjacent, one named barrier
-  // each): a tile's exchange overlaps its partner's sweeps. DTB_GROUPS=2
-  // forces it, =1 disables it; by default it is taken when it fits.
-  const char* ge = getenv("DTB_GROUPS");
-  const int gmode = ge ? atoi(ge) : 1;  // default off until measured
-  if (gmode != 1) {
-    const int K = elem == 8 ? 4 : 8, W = 4;
-    const int Lw_max = 32 * K;
-    const int64_t row_bytes = (int64_t)Lw_max * elem;
-    const int pairRows = (int)(dev.smem_optin / row_bytes);
-    for (int h : depths_for(depth)) {
-      const int hh = (int)std::min<int64_t>(h, std::max<int64_t>(steps, 1));
-      if (steps <= hh || h % 2) continue;  // only pays with exchanges; two-step sweeps
-      const int ntx_min = (int)((nx + 2 + Lw_max - 1) / Lw_max);
-      for (int ntx = std::max(1, ntx_min); ntx <= std::min<int64_t>(dev.sms, nx); ++ntx) {
-        Split sx;
-        if (!make_split((int)nx, ntx, h, K, Lw_max, ntx > 1 ? h : 1, sx, 0, 16 / elem)) continue;
-        const int nty_max = (int)std::min<int64_t>(dev.sms / ntx, ny / 2);
-        for (int nty = nty_max; nty >= std::max(1, nty_max - 2); --nty) {
-          Split sy;
-          if (!make_split((int)ny, 2 * nty, h, 1, pairRows, h, sy, 0, 1, 2)) continue;
-          int pair_max = 0;
-          for (int c = 0; c < nty; ++c)
-            pair_max = std::max(pair_max, (sy.l1[2 * c] - sy.l0[2 * c]) +
-                                              (sy.l1[2 * c + 1] - sy.l0[2 * c + 1]));
-          if (pair_max > pairRows) continue;
-          // cost: both tiles' sweeps back to back, the exchange hidden
-          const double cyc = tile_cycles(elem, K, 2 * W, pair_max, hh) + 0.15 * kExchangeLatency;
-          const double per_step = cyc / hh;
-          const double cpc = (double)nx * ny / per_step;
-          if (gmode == 2 || !found || cpc > best.cells_per_clk) {
-            if (gmode == 2 && found && best.groups == 2 && cpc <= best.cells_per_clk) continue;
-            found = true;
-            best.mode = 0;
-            best.elem = elem;
-            best.K = K;
-            best.warps = W;
-            best.groups = 2;
-            best.h = h;
-            best.sx = sx;
-            best.sy = sy;
-            best.ctas = ntx * nty;
-            best.ctas_per_sm = 1;
-            best.smem_bytes = (int64_t)pair_max * row_bytes;
             best.cycles_per_step = per_step;
             best.cells_per_clk = cpc;
           }
@@ -356,10 +272,7 @@ bool plan_streaming(int64_t nx, int64_t ny, int elem, int64_t steps, const DevIn
 // a few long segments so that there are about two pipelines' worth of
 // segments per SM.
 bool plan_pipe(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& dev, Plan& best) {
-#ifndef DTB_PIPE_WARPS
-#define DTB_PIPE_WARPS 16
-#endif
-  const int K = elem == 8 ? 4 : 8, W = DTB_PIPE_WARPS, S = DTB_PIPE_STAGES, P = W / S, h = 2 * S;
+  const int K = elem == 8 ? 4 : 8, W = kPlanPipeWarps, S = kPlanPipeStages, P = W / S, h = 2 * S;
   const int Lw_max = 32 * K;
   const int per = Lw_max - 2 * h;
   Split sx;
@@ -385,7 +298,7 @@ bool plan_pipe(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& d
   best.ctas = (int)std::min<int64_t>(dev.sms, (ntiles + P - 1) / P);
   best.ctas_per_sm = 1;
   // dtb_pipe.cuh PipeCfg: stage 0's prefetch ring is deeper for fp64
-  const int ring = W >= 16 ? 12 : 16, ring0 = (W >= 16 && elem == 8) ? 16 : ring;
+  const int ring = 12, ring0 = elem == 8 ? 16 : 12;
   best.smem_bytes = (int64_t)(ring0 + (S - 1) * ring) * Lw_max * elem * P;
   // cost: all lane-cells of every pass at ~70% of the FP issue rate + fill
   double lane_cells = 0;
@@ -404,27 +317,27 @@ bool plan_pipe(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& d
 
 static bool make_plan_search(int64_t nx, int64_t ny, int elem, int64_t steps,
                              const DevInfo& dev, int force, int depth, Plan& out, char* err,
-                             int errlen);
+                             int errlen, int64_t* min_bytes);
 
 // The planner's search (depths x tile counts x shapes) costs ~0.5 ms of host
 // time; solves of the same shape reuse the last plans (small MRU cache).
 bool make_plan(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& dev, int force,
-               int depth, Plan& out, char* err, int errlen) {
+               int depth, Plan& out, char* err, int errlen, int64_t* min_bytes) {
   struct Key {
     int64_t nx, ny, steps, smem_optin, l2, smem_sm;
-    int elem, force, depth, sms;
-    std::string shape;
+    int elem, force, depth, sms, max_tiles;
     bool operator==(const Key& o) const {
       return nx == o.nx && ny == o.ny && steps == o.steps && smem_optin == o.smem_optin &&
              l2 == o.l2 && smem_sm == o.smem_sm && elem == o.elem && force == o.force &&
-             depth == o.depth && sms == o.sms && shape == o.shape;
+             depth == o.depth && sms == o.sms && max_tiles == o.max_tiles;
     }
   };
   static std::mutex mu;
   static std::vector<std::pair<Key, Plan>> cache;  // most recent first
-  const char* sh = getenv("DTB_SHAPE");
+  const char* mt = getenv("DTB_MAX_TILES");
   const Key key{nx, ny, steps, dev.smem_optin, dev.l2_bytes, dev.smem_per_sm,
-                elem, force, depth, dev.sms, sh ? sh : ""};
+                elem, force, depth, dev.sms, mt ? atoi(mt) : 0};
+  if (min_bytes) *min_bytes = 0;
   {
     std::lock_guard<std::mutex> lk(mu);
     for (size_t i = 0; i < cache.size(); ++i) {
@@ -435,16 +348,34 @@ bool make_plan(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& d
       }
     }
   }
-  if (!make_plan_search(nx, ny, elem, steps, dev, force, depth, out, err, errlen)) return false;
+  if (!make_plan_search(nx, ny, elem, steps, dev, force, depth, out, err, errlen, min_bytes))
+    return false;
   std::lock_guard<std::mutex> lk(mu);
   cache.insert(cache.begin(), {key, out});
   if (cache.size() > 32) cache.pop_back();
   return true;
 }
 
+// Smallest shared memory per CTA that could hold a plan of this kind: the
+// streaming kernels need one tile of a single owned row plus its 2h halo rows
+// (a full lane-width row each); a resident plan needs the whole domain spread
+// over the device's CTAs with depth-h halos. Carried by
+// InfeasiblePlanError.min_required_bytes (planner.py:51-56, 222-228).
+static int64_t min_required_bytes(int64_t nx, int64_t ny, int elem, int h, const DevInfo& dev,
+                                  bool resident) {
+  const int K = elem == 8 ? 4 : 8;
+  const int64_t row_bytes = 32LL * K * elem;
+  if (!resident) return std::min<int64_t>(1 + 2LL * h, ny + 2) * row_bytes;
+  const int64_t per = std::max<int64_t>(1, 32LL * K - 2LL * h);
+  const int64_t ntx = std::max<int64_t>(1, (nx + per - 1) / per);
+  const int64_t nty = std::max<int64_t>(1, dev.sms / ntx);
+  const int64_t rows = (ny + 2 + 2LL * h * (nty - 1) + nty - 1) / nty;
+  return rows * row_bytes;
+}
+
 static bool make_plan_search(int64_t nx, int64_t ny, int elem, int64_t steps,
                              const DevInfo& dev, int force, int depth, Plan& out, char* err,
-                             int errlen) {
+                             int errlen, int64_t* min_bytes) {
   if (nx < 1 || ny < 1) {
     snprintf(err, errlen, "domain dims must be at least 1x1, got %lldx%lld", (long long)nx,
              (long long)ny);
@@ -473,14 +404,18 @@ static bool make_plan_search(int64_t nx, int64_t ny, int elem, int64_t steps,
     // streaming kernel on B200: 0.85 vs 0.64 Tcells/s fp64 at 16384^2), with
     // the tile sweep as the fallback (a forced depth other than 8, tiny grids)
     ok = plan_resident(nx, ny, elem, steps, dev, depth, p);
-    if (!ok && (depth == 0 || depth == 2 * DTB_PIPE_STAGES) && nx >= 64 && ny >= 64)
+    if (!ok && (depth == 0 || depth == 2 * kPlanPipeStages) && nx >= 64 && ny >= 64)
       ok = plan_pipe(nx, ny, elem, steps, dev, p);
     if (!ok) ok = plan_streaming(nx, ny, elem, steps, dev, depth, p);
   }
   if (!ok) {
+    const int h = depth > 0 ? depth : 2;
+    const int64_t need = min_required_bytes(nx, ny, elem, h, dev, force == 4);
+    if (min_bytes) *min_bytes = need;
     snprintf(err, errlen,
-             "no B200 tiling fits %lldx%lld (elem %d B, depth %d) in %lld B of shared memory per CTA",
-             (long long)nx, (long long)ny, elem, depth, (long long)dev.smem_optin);
+             "no B200 tiling fits %lldx%lld (elem %d B, depth %d) in %lld B of shared memory per "
+             "CTA: needs at least %lld B",
+             (long long)nx, (long long)ny, elem, depth, (long long)dev.smem_optin, (long long)need);
     return false;
   }
   // lane-cells updated per step (every inner cell of every load region)

@@ -41,7 +41,7 @@ struct DevInfo {
 };
 
 struct Plan {
-  int mode = 0;  // 0 resident, 1 streaming, 2 naive
+  int mode = 0;  // 0 resident, 1 streaming (tile sweep), 2 naive, 3 pipelined streaming
   int elem = 8;
   int K = 4;
   int warps = 16;
@@ -49,7 +49,6 @@ struct Plan {
   Split sx, sy;
   int ctas = 0;
   int ctas_per_sm = 1;
-  int groups = 1;       // resident: tiles per CTA (vertically adjacent, one warp group each)
   int64_t smem_bytes = 0;
   double cycles_per_step = 0;  // cost model
   double cells_per_clk = 0;
@@ -68,9 +67,12 @@ struct Plan {
 bool make_split(int N, int n, int h, int align, int maxL, int min_owned, Split& s,
                 int off = 0, int start_align = 1, int spread = 1);
 
-// Choose the execution plan. force: 0 auto, 1 streaming, 2 naive.
-// depth > 0 pins the halo depth.
+// Choose the execution plan. force: 0 auto, 1 streaming, 2 naive, 3 pipelined,
+// 4 resident. depth > 0 pins the halo depth. On failure, err holds the message
+// and *min_bytes (if non-null) the smallest per-CTA shared memory a plan of the
+// requested kind would need.
 bool make_plan(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& dev,
-               int force, int depth, Plan& out, char* err, int errlen);
+               int force, int depth, Plan& out, char* err, int errlen,
+               int64_t* min_bytes = nullptr);
 
 }  // namespace dtb

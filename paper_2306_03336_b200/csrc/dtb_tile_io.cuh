@@ -1,0 +1,199 @@
+// dtb_tile_io.cuh — global <-> shared tile movement for the resident and
+// tile-streaming kernels: whole-tile loads/stores, the resident halo refresh
+// (per-neighbour epoch flags), and the NaN-poison debug mode.
+#pragma once
+#include "dtb_core.cuh"
+
+namespace dtb {
+
+__device__ __forceinline__ void cp_async(uint32_t dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async(uint32_t dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Whole-rectangle tile copies, one warp per row, one 16-byte smem chunk per
+// lane-iteration: tile rows [r0, r1) x cols [c0, c1) <-> global padded
+// (gy0 + r, gx0 + c). When the global side is 16-byte aligned chunk-for-chunk
+// (gx0 and pitch multiples of the chunk), whole chunks move as one 16-byte
+// cp.async / STG; otherwise element by element. Loads are cp.async (the
+// caller waits and synchronises).
+template <typename T, int K>
+__device__ __forceinline__ void g2s_rows(T* tile, const T* __restrict__ g, int64_t pitch, int gx0,
+                                         int gy0, int r0, int r1, int c0, int c1) {
+  typedef Tile<T, K> L;
+  constexpr int E = L::EPC;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const bool vec = ((gx0 % E) == 0) && ((pitch % E) == 0);
+  const int q0 = c0 / E, q1 = (c1 + E - 1) / E;
+  for (int r = r0 + warp; r < r1; r += nw) {
+    const T* src = g + (int64_t)(gy0 + r) * pitch + gx0;
+    const uint32_t srow = sbase + (uint32_t)(r * L::ROW * (int)sizeof(T));
+    for (int q = q0 + lane; q < q1; q += 32) {
+      const uint32_t sa = srow + (uint32_t)(L::swz(q) * 16);
+      const int cb = q * E;
+      if (vec && cb >= c0 && cb + E <= c1) {
+        cp_async16(sa, src + cb);
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          if (cb + e >= c0 && cb + e < c1) cp_async(sa + (uint32_t)(e * sizeof(T)), src + cb + e);
+      }
+    }
+  }
+}
+
+template <typename T, int K>
+__device__ __forceinline__ void s2g_rows(const T* tile, T* __restrict__ g, int64_t pitch, int gx0,
+                                         int gy0, int r0, int r1, int c0, int c1) {
+  typedef Tile<T, K> L;
+  typedef typename Arith<T>::vec_t V;
+  constexpr int E = L::EPC;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const bool vec = ((gx0 % E) == 0) && ((pitch % E) == 0);
+  const int q0 = c0 / E, q1 = (c1 + E - 1) / E;
+  for (int r = r0 + warp; r < r1; r += nw) {
+    T* dst = g + (int64_t)(gy0 + r) * pitch + gx0;
+    const T* srow = tile + r * L::ROW;
+    for (int q = q0 + lane; q < q1; q += 32) {
+      const V x = *reinterpret_cast<const V*>(srow + L::swz(q) * E);
+      const T* px = reinterpret_cast<const T*>(&x);
+      const int cb = q * E;
+      if (vec && cb >= c0 && cb + E <= c1) {
+        *reinterpret_cast<V*>(dst + cb) = x;
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          if (cb + e >= c0 && cb + e < c1) dst[cb + e] = px[e];
+      }
+    }
+  }
+}
+
+// Copy tile rect [r0, r1) x [c0, c1) from global by 16-byte smem chunks,
+// flattened over (row, chunk) across the 32 lanes of one warp. Whole chunks
+// use a 16-byte cp.async when the global side is aligned (vec).
+template <typename T, int K>
+__device__ __forceinline__ void warp_g2s_chunks(uint32_t sbase, const T* __restrict__ g,
+                                                int64_t pitch, int gx0, int gy0, int r0, int r1,
+                                                int c0, int c1, bool vec, int lane) {
+  typedef Tile<T, K> L;
+  constexpr int E = L::EPC;
+  const int q0 = c0 / E, nq = (c1 + E - 1) / E - q0, n = (r1 - r0) * nq;
+  if (n <= 0) return;
+  const uint64_t m = (0xFFFFFFFFull + (uint64_t)nq) / (uint64_t)nq;
+  for (int i = lane; i < n; i += 32) {
+    const uint32_t rr = (uint32_t)(((uint64_t)(uint32_t)i * m) >> 32);
+    const int r = r0 + (int)rr, q = q0 + i - (int)rr * nq, cb = q * E;
+    const uint32_t sa = sbase + (uint32_t)((r * L::ROW + L::swz(q) * E) * (int)sizeof(T));
+    const T* src = g + (int64_t)(gy0 + r) * pitch + gx0 + cb;
+    if (vec && cb >= c0 && cb + E <= c1) {
+      cp_async16(sa, src);
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (cb + e >= c0 && cb + e < c1) cp_async(sa + (uint32_t)(e * sizeof(T)), src + e);
+    }
+  }
+}
+
+// Resident halo refresh, warp-specialised by direction: the ring is cut into
+// 8 regions (N, S, the 4 corners, W, E), each owned by one neighbour; warp k
+// polls that neighbour's epoch flag (acquire) and streams its region in with
+// cp.async as soon as it is published, so the waits and loads of the eight
+// directions overlap. `mark` (tracing): when warp 0's first flag arrived.
+template <typename T, int K>
+__device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restrict__ g,
+                                                     int64_t pitch, int gx0, int gy0,
+                                                     const int* flags, int epoch, int ntx, int nty,
+                                                     int tx, int ty, int ry0, int oy0, int oy1,
+                                                     int ry1, int rx0, int ox0, int ox1, int rx1,
+                                                     unsigned long long* mark = nullptr) {
+  typedef Tile<T, K> L;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const bool vec = ((gx0 % L::EPC) == 0) && ((pitch % L::EPC) == 0);
+  int polled = -1;  // neighbour this warp last waited for
+  for (int k = warp; k < 8; k += nw) {
+    int dx, dy, r0, r1, c0, c1;
+    switch (k) {
+      case 0: dx = 0; dy = -1; r0 = ry0; r1 = oy0; c0 = ox0; c1 = ox1; break;
+      case 1: dx = 0; dy = 1; r0 = oy1; r1 = ry1; c0 = ox0; c1 = ox1; break;
+      case 2: dx = -1; dy = -1; r0 = ry0; r1 = oy0; c0 = rx0; c1 = ox0; break;
+      case 3: dx = 1; dy = -1; r0 = ry0; r1 = oy0; c0 = ox1; c1 = rx1; break;
+      case 4: dx = -1; dy = 1; r0 = oy1; r1 = ry1; c0 = rx0; c1 = ox0; break;
+      case 5: dx = 1; dy = 1; r0 = oy1; r1 = ry1; c0 = ox1; c1 = rx1; break;
+      case 6: dx = -1; dy = 0; r0 = oy0; r1 = oy1; c0 = rx0; c1 = ox0; break;
+      default: dx = 1; dy = 0; r0 = oy0; r1 = oy1; c0 = ox1; c1 = rx1; break;
+    }
+    const int nxt = tx + dx, nyt = ty + dy;
+    if (r1 <= r0 || c1 <= c0 || nxt < 0 || nxt >= ntx || nyt < 0 || nyt >= nty) continue;
+    const int nb = nyt * ntx + nxt;
+    if (nb != polled) {
+      if (lane == 0)
+        while (ld_acquire_gpu(flags + nb) < epoch) __nanosleep(32);
+      __syncwarp();
+      if (mark && polled < 0) *mark = clock64();
+      polled = nb;
+    }
+    warp_g2s_chunks<T, K>(sbase, g, pitch, gx0, gy0, r0, r1, c0, c1, vec, lane);
+  }
+  cp_async_wait_all();
+}
+
+// Poison (debug, DTB_FLAG_POISON): NaN every tile cell a correct schedule can
+// no longer read after `done` steps of the epoch — the ring of width `done`
+// along halo sides (the trapezoid rim, planner.py:272-286) plus the unused
+// lane columns. A stale read anywhere then propagates NaN into the owned
+// cells and fails the bitwise comparison (the reference's poison mode,
+// engine.py:16-20,174-177).
+template <typename T, int K>
+__device__ void poison_rim(T* tile, int Lw, int Lh, int done, bool hl, bool hr, bool ht, bool hb) {
+  typedef Tile<T, K> L;
+  const T nanv = (T)NAN;
+  for (int i = threadIdx.x; i < Lh * L::ROW; i += blockDim.x) {
+    const int r = i / L::ROW, c = i % L::ROW;
+    bool p = c >= Lw;
+    p |= hl && c < done;
+    p |= hr && c >= Lw - done;
+    p |= ht && r < done;
+    p |= hb && r >= Lh - done;
+    if (p) tile[L::at(r, c)] = nanv;
+  }
+}
+
+// advance_tile, or in poison mode one step at a time with the stale rim
+// NaN-ed after each step
+template <typename T, int K, bool SYM, bool DYN>
+__device__ void advance(T* tile, int Lw, int Lh, int steps, const Weights<T>& wt, bool poison,
+                        bool hl, bool hr, bool ht, bool hb,
+                        const Publisher<T, K>* pub = nullptr) {
+  if (!poison) {
+    advance_tile<T, K, SYM, DYN>(tile, Lw, Lh, steps, wt, pub);
+    return;
+  }
+  for (int s = 0; s < steps; ++s) {
+    advance_tile<T, K, SYM, DYN>(tile, Lw, Lh, 1, wt);
+    poison_rim<T, K>(tile, Lw, Lh, s + 1, hl, hr, ht, hb);
+    __syncthreads();
+  }
+}
+
+}  // namespace dtb

@@ -52,7 +52,7 @@ def _raise(rc: int):
     if rc == _native.DTB_ERANGE:
         raise IndexError(msg)
     if rc == _native.DTB_EINFEASIBLE:
-        raise InfeasiblePlanError(msg, 0)
+        raise InfeasiblePlanError(msg, int(_native.lib().dtb_last_min_required_bytes()))
     raise EngineError(msg)
 
 
@@ -186,29 +186,34 @@ def j2d5pt_device(src, dst, nx: int, ny: int, weights, steps: int, *, valid=None
     and ``dst`` are padded (ny+2, pitch) float64/float32 buffers on the
     current device; runs on ``stream`` (default: torch's current stream)."""
     import torch
-    if isinstance(src, torch.Tensor):
-        if src.dtype != dst.dtype or src.shape != dst.shape or not src.is_cuda:
-            raise ValueError("src/dst must be CUDA tensors of equal dtype and shape")
-        if src.dim() != 2 or src.shape[0] != ny + 2 or src.shape[1] < nx + 2:
-            raise ValueError(f"expected ({ny + 2}, >= {nx + 2}) buffers, got {tuple(src.shape)}")
-        if src.stride(1) != 1 or dst.stride() != src.stride():
-            raise ValueError("buffers must be row-major with equal strides")
-        pitch = src.stride(0)
-        tag, ctype = ("f64", ctypes.c_double) if src.dtype == torch.float64 else ("f32", ctypes.c_float)
-        pin, pout = src.data_ptr(), dst.data_ptr()
-        if stream is None:
-            stream = torch.cuda.current_stream(src.device).cuda_stream
-    else:
+    if not isinstance(src, torch.Tensor) or not isinstance(dst, torch.Tensor):
         raise TypeError("j2d5pt_device expects torch CUDA tensors")
+    if src.dtype not in (torch.float64, torch.float32):
+        raise ValueError(f"src/dst dtype must be float64 or float32, got {src.dtype}")
+    if src.dtype != dst.dtype or src.shape != dst.shape or not src.is_cuda:
+        raise ValueError("src/dst must be CUDA tensors of equal dtype and shape")
+    if dst.device != src.device:
+        raise ValueError(f"src is on {src.device}, dst on {dst.device}")
+    if src.dim() != 2 or src.shape[0] != ny + 2 or src.shape[1] < nx + 2:
+        raise ValueError(f"expected ({ny + 2}, >= {nx + 2}) buffers, got {tuple(src.shape)}")
+    if src.stride(1) != 1 or dst.stride() != src.stride():
+        raise ValueError("buffers must be row-major with equal strides")
+    pitch = src.stride(0)
+    tag, ctype = ("f64", ctypes.c_double) if src.dtype == torch.float64 else ("f32", ctypes.c_float)
+    pin, pout = src.data_ptr(), dst.data_ptr()
     w = (ctype * 5)(*as_weights_tuple(weights))
     if depth is not None:
         flags |= _native.FLAG_FORCE_DEPTH
     rep = _native.DtbReport()
     vr = _rect(valid)
     fn = getattr(_native.lib(), f"dtb_j2d5pt_{tag}_dev")
-    rc = fn(pin, pout, nx, ny, pitch, w, steps, depth if depth is not None else 1,
-            ctypes.byref(vr) if vr is not None else None, flags, ctypes.c_void_p(stream),
-            ctypes.byref(rep))
+    # the library plans, allocates scratch and launches on the current device
+    with torch.cuda.device(src.device):
+        if stream is None:
+            stream = torch.cuda.current_stream(src.device).cuda_stream
+        rc = fn(pin, pout, nx, ny, pitch, w, steps, depth if depth is not None else 1,
+                ctypes.byref(vr) if vr is not None else None, flags, ctypes.c_void_p(stream),
+                ctypes.byref(rep))
     if rc != _native.DTB_OK:
         _raise(rc)
     return _report(rep)

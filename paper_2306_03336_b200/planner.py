@@ -229,7 +229,7 @@ def plan_b200(nx: int, ny: int, elem_bytes: int = 8, total_steps: int = 1, t_dep
     if rc != _native.DTB_OK:
         msg = _native.last_error()
         if rc == _native.DTB_EINFEASIBLE:
-            raise InfeasiblePlanError(msg, 0)
+            raise InfeasiblePlanError(msg, int(_native.lib().dtb_last_min_required_bytes()))
         raise ValueError(msg)
     return B200Plan(MODES[info.mode], info.elem_bytes, info.lane_elems, info.warps, info.halo,
                     info.tiles_x, info.tiles_y, info.ctas, info.ctas_per_sm, bool(info.dyn),

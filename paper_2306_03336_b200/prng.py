@@ -79,16 +79,29 @@ class Xoshiro256StarStar:
         return seq[self.randint(0, len(seq) - 1)]
 
 
+def _check_fill_buffer(buf, nx: int, ny: int, rows: int, dtypes):
+    import torch
+    if not isinstance(buf, torch.Tensor) or not buf.is_cuda:
+        raise TypeError("expected a CUDA tensor")
+    if buf.dtype not in dtypes:
+        raise ValueError(f"buffer dtype must be one of {[str(d) for d in dtypes]}, got {buf.dtype}")
+    if buf.dim() != 2 or buf.stride(1) != 1 or buf.shape[0] < rows or buf.shape[1] < nx + 2:
+        raise ValueError(f"expected a row-major ({rows}, >= {nx + 2}) buffer, got "
+                         f"{tuple(buf.shape)} with strides {buf.stride()}")
+
+
 def fill_random_device(buf, nx: int, ny: int, seed: int, ghost: float = 0.0, stream=None):
     """Fill a padded (ny+2, pitch) CUDA tensor like grid_new(nx, ny, random_interior(...), ghost)."""
     import torch
     from . import _native
-    if stream is None:
-        stream = torch.cuda.current_stream(buf.device).cuda_stream
-    fn = _native.lib().dtb_fill_random_f64 if buf.dtype == torch.float64 else \
-        _native.lib().dtb_fill_random_f32
-    rc = fn(buf.data_ptr(), nx, ny, buf.stride(0), seed & (2 ** 64 - 1), float(ghost),
-            ctypes.c_void_p(stream))
+    _check_fill_buffer(buf, nx, ny, ny + 2, (torch.float64, torch.float32))
+    with torch.cuda.device(buf.device):
+        if stream is None:
+            stream = torch.cuda.current_stream(buf.device).cuda_stream
+        fn = _native.lib().dtb_fill_random_f64 if buf.dtype == torch.float64 else \
+            _native.lib().dtb_fill_random_f32
+        rc = fn(buf.data_ptr(), nx, ny, buf.stride(0), seed & (2 ** 64 - 1), float(ghost),
+                ctypes.c_void_p(stream))
     if rc != 0:
         raise RuntimeError(_native.last_error())
 
@@ -98,10 +111,12 @@ def fill_random_rows_device(buf, nx: int, ny: int, seed: int, row0: int, ghost: 
     """Rows [row0, row0 + buf.shape[0]) of the padded fp64 random grid into ``buf``."""
     import torch
     from . import _native
-    if stream is None:
-        stream = torch.cuda.current_stream(buf.device).cuda_stream
-    rc = _native.lib().dtb_fill_random_rows_f64(buf.data_ptr(), nx, ny, buf.stride(0),
-                                                 seed & (2 ** 64 - 1), float(ghost), row0,
-                                                 buf.shape[0], ctypes.c_void_p(stream))
+    _check_fill_buffer(buf, nx, ny, 0, (torch.float64,))
+    with torch.cuda.device(buf.device):
+        if stream is None:
+            stream = torch.cuda.current_stream(buf.device).cuda_stream
+        rc = _native.lib().dtb_fill_random_rows_f64(buf.data_ptr(), nx, ny, buf.stride(0),
+                                                     seed & (2 ** 64 - 1), float(ghost), row0,
+                                                     buf.shape[0], ctypes.c_void_p(stream))
     if rc != 0:
         raise RuntimeError(_native.last_error())

@@ -181,3 +181,23 @@ def test_native_validation_errors_without_gpu():
 def test_weights_validation():
     with pytest.raises(ValueError):
         StencilWeights(0.2, 0.2, float("inf"), 0.2, 0.2)
+
+
+def test_infeasible_plan_carries_min_required_bytes():
+    """InfeasiblePlanError(msg, min_required_bytes) (planner.py:51-56,222-228):
+    the B200 planner reports the smallest per-CTA shared memory a plan of the
+    requested kind would need, through dtb_last_min_required_bytes."""
+    from paper_2306_03336_b200 import InfeasiblePlanError
+    # 16384^2 fp64 cannot be smem-resident on one B200 (2.1 GB vs 34 MB)
+    with pytest.raises(InfeasiblePlanError) as ei:
+        plan_b200(16384, 16384, 8, 100, 1, _native.FLAG_FORCE_RESIDENT)
+    need = ei.value.min_required_bytes
+    assert need > 232448, need
+    assert str(need) in str(ei.value)
+    # a forced depth whose halo rows alone overflow a CTA's shared memory
+    with pytest.raises(InfeasiblePlanError) as ei:
+        plan_b200(4096, 4096, 8, 400, 200, _native.FLAG_FORCE_STREAM | _native.FLAG_FORCE_DEPTH)
+    assert ei.value.min_required_bytes == (1 + 2 * 200) * 1024
+    # success clears it
+    plan_b200(256, 256, 8, 100, 1)
+    assert _native.lib().dtb_last_min_required_bytes() == 0
