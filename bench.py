@@ -9,9 +9,18 @@ Jacobi steps of a 1900^2 fp64 grid), inputs already resident in HBM
 reference's random_interior). Metric (BASELINE.json): GCells/s = valid
 cell-updates nx*ny*steps per second. Prints ONE JSON line on rank 0.
 
---impl reference times the reference's CPU algorithm (the pinned numpy
-restatement of jacobi_reference in oracle/, single-threaded by contract) on
-a bounded sample of the same workload on this host.
+--impl reference times the reference's CPU algorithm on this host's cores:
+the C restatement of jacobi_reference (oracle/j2d5pt_oracle.c, bitwise pinned
+to the reference, pthreads over all host cores) on a bounded sample of the
+same workload. The b200 line's cpu_baseline carries the same port plus the
+BASELINE.md §4 legs with the reference's own structure (oracle/engine_port.py):
+jacobi_reference's row-wise numpy loop on one pinned core, and the reference
+DTB engine (run_dtb) with the B200 DeviceModel at threads=1 and threads=cores.
+
+--gpus N > 1 runs the C5 weak-scaling series (32768 x 4096N fp64 y-slabs, one
+rank per GPU, depth-16 halos) plus strong scaling at the fixed 32768^2; the
+N=1 line (C2 headline) carries the same family's N=1 anchors under "c5".
+Without a launcher, --gpus N > 1 re-launches itself under torch.distributed.run.
 """
 
 from __future__ import annotations
@@ -169,9 +178,62 @@ def _cpu_port():
             f"numpy port (1 core, {model})"
 
 
-def cpu_reference_sample(nx, ny, dtype, budget_s=10.0):
+def _reference_legs(nx, ny):
+    """BASELINE.md §4 legs with the reference's own structure
+    (oracle/engine_port.py, bitwise-pinned to the reference's outputs):
+    jacobi_reference's row-wise numpy loop on ONE pinned core, and the
+    reference DTB engine run_dtb with the B200 DeviceModel (148 workers x
+    232448 B) at threads=1 and threads=host cores, each on a bounded sample
+    of whole time blocks (per-step cost is constant, so the rate carries)."""
+    import numpy as np
+    from oracle.engine_port import jacobi_rowwise, run_dtb_port
+    from paper_2306_03336_b200 import DeviceModel, plan_device_tiles
+    from paper_2306_03336_b200.grid import grid_new
+    from paper_2306_03336_b200.prng import random_interior
+    g = grid_new(nx, ny, random_interior(nx, ny, 1)).data
+    w = (0.2, 0.2, 0.2, 1.0 - 4 * 0.2, 0.2)
+    cores = os.cpu_count() or 1
+    legs = []
+    # 1. jacobi_reference on one core (single-threaded by contract, SPEC.md:169,178)
+    try:
+        old = os.sched_getaffinity(0)
+        pin = min(old)
+        os.sched_setaffinity(0, {pin})
+    except (AttributeError, OSError):
+        old, pin = None, None
+    try:
+        t0 = time.perf_counter()
+        jacobi_rowwise(g, w, 2)
+        per = (time.perf_counter() - t0) / 2
+        k = max(2, min(200, int(4.0 / per)))
+        t0 = time.perf_counter()
+        jacobi_rowwise(g, w, k)
+        el = time.perf_counter() - t0
+    finally:
+        if old is not None:
+            os.sched_setaffinity(0, old)
+    legs.append({"leg": "jacobi_reference (oracle.py:19-34), row-wise numpy, 1 core"
+                        + (f" (pinned to cpu {pin})" if pin is not None else ""),
+                 "value": nx * ny * k / el / 1e9, "unit": "GCells/s", "cores": 1,
+                 "sample": f"{nx}x{ny} f64, {k} steps, {el:.1f} s"})
+    # 2. run_dtb (engine.py:305-326) with the B200 DeviceModel, one time block of T=2
+    plan = plan_device_tiles((nx, ny), DeviceModel("b200", 148, 232448), 2)
+    for threads in sorted({1, cores}):
+        t0 = time.perf_counter()
+        run_dtb_port(g, w, 2, plan, threads)
+        el = time.perf_counter() - t0
+        legs.append({"leg": f"run_dtb (engine.py:305-326), B200 DeviceModel 148 x 232448 B, "
+                            f"t_depth 2, threads={threads}",
+                     "value": nx * ny * 2 / el / 1e9, "unit": "GCells/s", "cores": threads,
+                     "sample": f"{nx}x{ny} f64, one time block of 2 steps over "
+                               f"{len(plan.tiles)} tiles, {el:.1f} s"})
+    return legs
+
+
+def cpu_reference_sample(nx, ny, dtype, budget_s=8.0, legs=True):
     """Time the reference algorithm (a bitwise-pinned CPU port of
-    jacobi_reference, oracle.py:19-34) on this host's cores."""
+    jacobi_reference, oracle.py:19-34) on all of this host's cores; with
+    `legs`, also the reference-structured BASELINE.md §4 legs."""
     import numpy as np
     from paper_2306_03336_b200.grid import grid_new
     from paper_2306_03336_b200.prng import random_interior
@@ -193,10 +255,13 @@ def cpu_reference_sample(nx, ny, dtype, budget_s=10.0):
     t0 = time.perf_counter()
     run(g.data, w, steps, dt)
     el = time.perf_counter() - t0
-    return {"value": nx * ny * steps / el / 1e9, "unit": "GCells/s", "cores": cores,
-            "kind": "port",
-            "sample": f"{nx}x{ny} {dtype}, {steps} steps of the {what} restatement of "
-                      f"jacobi_reference (oracle/, pinned to the reference), {el:.1f} s"}
+    out = {"value": nx * ny * steps / el / 1e9, "unit": "GCells/s", "cores": cores,
+           "kind": "port",
+           "sample": f"{nx}x{ny} {dtype}, {steps} steps of the {what} restatement of "
+                     f"jacobi_reference (oracle/, pinned to the reference), {el:.1f} s"}
+    if legs:
+        out["legs"] = _reference_legs(nx, ny)
+    return out
 
 
 def run_reference(args):
@@ -247,24 +312,19 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def run_slab(args, world, rank, local):
-    """C5: one y-slab per rank (SlabSolver), halo rows exchanged point-to-point
-    over NCCL every `depth` steps; weak scaling (4096 rows per GPU)."""
+def slab_series(args, world, rank, local, ny, steps, exchange="auto"):
+    """One C5-family measurement: a 32768 x ny fp64 domain in `world` y-slabs,
+    one per rank (SlabSolver), depth-16 halos. Returns the whole-job rate
+    (max over ranks) and the e2e leg, or None on ranks != 0."""
     import torch
     import torch.distributed as dist
     from paper_2306_03336_b200 import StencilWeights, j2d5pt_device, last_launch_count
     from paper_2306_03336_b200.prng import fill_random_rows_device
     from paper_2306_03336_b200.slab import SlabGeometry, SlabSolver
-    nx, rows_per_gpu, steps, dtype, desc = WORKLOADS["c5"]
-    if args.solve_steps:
-        steps = args.solve_steps
-    ny = rows_per_gpu * world
-    depth = 16
+    nx, depth = WORKLOADS["c5"][0], 16
     dev = torch.device("cuda", local)
     geo = SlabGeometry(nx, ny, world, rank, depth)
     pitch = (nx + 2 + 31) // 32 * 32
-    a = torch.empty((geo.local_ny + 2, pitch), dtype=torch.float64, device=dev)
-    b = torch.empty_like(a)
     w = StencilWeights.diffusive(0.2)
     launches = [0]
 
@@ -272,7 +332,9 @@ def run_slab(args, world, rank, local):
         j2d5pt_device(src, dst, lnx, lny, w, k)
         launches[0] += last_launch_count()
 
-    solver = SlabSolver(geo, local_solve, dist if world > 1 else None)
+    solver = SlabSolver(geo, local_solve, dist if world > 1 else None, exchange=exchange,
+                        weights=w.astuple())
+    a, b = solver.allocate(pitch, torch.float64, dev)
 
     def fresh():
         fill_random_rows_device(a, nx, ny, 1, geo.global_row0)
@@ -289,6 +351,7 @@ def run_slab(args, world, rank, local):
     stream = torch.cuda.current_stream(dev)
     total_ms = 0.0
     launches[0] = 0
+    solver.launches = 0
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             fresh()
@@ -301,8 +364,9 @@ def run_slab(args, world, rank, local):
             torch.cuda.synchronize()
             barrier()
             total_ms += s.elapsed_time(e)
+    launches_timed = launches[0] + solver.launches
     # e2e through the same public API: each rank's slab from pinned host
-    # memory (H2D), the slab solve with its NCCL halo exchanges, the owned rows
+    # memory (H2D), the slab solve with its halo exchanges, the owned rows
     # back (D2H), all inside the timed window
     fresh()
     torch.cuda.synchronize()
@@ -327,38 +391,61 @@ def run_slab(args, world, rank, local):
         t = torch.tensor([total_ms, e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, e2e_ms = float(t[0].item()), float(t[1].item())
+    mode = solver.exchange_mode
+    solver.close()
+    del a, b
+    torch.cuda.empty_cache()
+    if rank != 0:
+        return None
     cells = nx * ny * steps  # whole job
-    value = cells * args.steps / (total_ms * 1e-3) / 1e9
-    e2e = {"value": cells * args.steps / (e2e_ms * 1e-3) / 1e9, "unit": "GCells/s",
-           "h2d_bytes_per_step": int(h_in.numel() * h_in.element_size()) * world,
-           "d2h_bytes_per_step": int(h_out.numel() * h_out.element_size()) * world,
-           "api": "paper_2306_03336_b200.slab.SlabSolver over j2d5pt_device "
-                  "(dtb_j2d5pt_f64_dev), pinned host buffers per rank"}
+    return {
+        "value": cells * args.steps / (total_ms * 1e-3) / 1e9, "unit": "GCells/s",
+        "ms_per_step": total_ms / args.steps, "nx": nx, "ny": ny, "solve_steps": steps,
+        "n_gpus": world, "depth": depth, "exchange": mode,
+        "gpu_launches": launches_timed,
+        "clocks": clk.summary(),
+        "nvlink_halo_bytes_per_exchange_per_gpu":
+            2 * depth * (nx + 2) * 8 * (2 if world > 2 else 1) if world > 1 else 0,
+        "e2e": {"value": cells * args.steps / (e2e_ms * 1e-3) / 1e9, "unit": "GCells/s",
+                "h2d_bytes_per_step": int(h_in.numel() * h_in.element_size()) * world,
+                "d2h_bytes_per_step": int(h_out.numel() * h_out.element_size()) * world,
+                "api": "paper_2306_03336_b200.slab.SlabSolver over j2d5pt_device "
+                       "(dtb_j2d5pt_f64_dev), pinned host buffers per rank"},
+    }
+
+
+def run_slab(args, world, rank, local):
+    """N > 1 (or --workload c5): the C5 weak series 32768 x (4096 N), plus
+    strong scaling at the fixed 32768^2 under "strong"."""
+    nx, rows_per_gpu, steps, dtype, desc = WORKLOADS["c5"]
+    if args.solve_steps:
+        steps = args.solve_steps
+    weak = slab_series(args, world, rank, local, rows_per_gpu * world, steps)
+    strong = None if args.no_strong else slab_series(args, world, rank, local, nx, steps)
     if rank != 0:
         return
     peaks = measured_peaks()
-    per_gpu = value / world
-    rooflines = {
-        "fp_pipe": {"achieved": per_gpu * 9, "peak": peaks["fp64_gops"], "unit": "Gop/s",
-                    "ops_per_cell": 9},
-    }
-    rooflines["fp_pipe"]["frac"] = rooflines["fp_pipe"]["achieved"] / rooflines["fp_pipe"]["peak"]
-    halo_bytes = 2 * depth * (nx + 2) * 8 * (2 if world > 2 else 1)
+    per_gpu = weak["value"] / world
+    ops = 6  # diffusive weights: the isotropic shared-product form (dtb_core.cuh)
+    fp = {"achieved": per_gpu * ops, "peak": peaks["fp64_gops"], "unit": "Gop/s",
+          "ops_per_cell": ops, "frac": per_gpu * ops / peaks["fp64_gops"]}
     line = {
-        "metric": METRIC, "value": value, "unit": "GCells/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "metric": METRIC, "value": weak["value"], "unit": "GCells/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": weak["ms_per_step"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
         "data": "synthetic (splitmix64 random_interior seed 1, each slab filled on its GPU)",
-        "config": {"workload": desc, "nx": nx, "ny": ny, "solve_steps": steps, "depth": depth,
-                   "parallelism": f"y-slab x{world}", "l2": "inputs (>= 1 GB) larger than L2"},
-        "roofline": dict(rooflines["fp_pipe"], bound="fp64_pipe", traffic=None),
-        "rooflines": rooflines,
-        "nvlink_halo_bytes_per_exchange_per_gpu": halo_bytes if world > 1 else 0,
-        "gpu_launches": launches[0],
-        "clocks": clk.summary(),
-        "e2e": e2e,
+        "config": {"workload": desc, "nx": nx, "ny": weak["ny"], "solve_steps": steps,
+                   "depth": weak["depth"], "parallelism": f"y-slab x{world}",
+                   "exchange": weak["exchange"], "l2": "inputs (>= 1 GB) larger than L2"},
+        "roofline": dict(fp, bound="fp64_pipe", kernel="pipe_kernel", traffic=None),
+        "rooflines": {"fp_pipe": fp},
+        "nvlink_halo_bytes_per_exchange_per_gpu": weak["nvlink_halo_bytes_per_exchange_per_gpu"],
+        "gpu_launches": weak["gpu_launches"],
+        "clocks": weak["clocks"],
+        "e2e": weak["e2e"],
+        "strong": strong,
         # the CPU leg runs at N=1 only (bench contract)
-        "cpu_baseline": (cpu_reference_sample(nx, 256, dtype)
+        "cpu_baseline": (cpu_reference_sample(1900, 1900, dtype)
                          if not args.no_cpu and world == 1 else None),
     }
     print(json.dumps(line), flush=True)
@@ -374,11 +461,29 @@ def run_b200(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if world > 1 or args.workload == "c5":
         return run_slab(args, world, rank, local)
+    line = run_single(args, world, rank, local)
+    # the C5 family's N=1 anchors (the series --gpus N > 1 runs), measured
+    # after the headline (the pipelined kernel runs at the power cap)
+    if line is not None and args.workload == "c2" and not args.no_c5:
+        c5_steps = args.solve_steps or WORKLOADS["c5"][2]
+        line["c5"] = {"weak_n1": slab_series(args, 1, 0, local, WORKLOADS["c5"][1], c5_steps),
+                      "strong_32768_n1": None if args.no_strong else
+                      slab_series(args, 1, 0, local, WORKLOADS["c5"][0], c5_steps)}
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+def run_single(args, world, rank, local):
+    """The single-GPU workload line (C2 headline by default); None off rank 0."""
+    import numpy as np
+    import torch
     from paper_2306_03336_b200 import StencilWeights, j2d5pt_device, last_launch_count, plan_b200
     from paper_2306_03336_b200 import _native
     from paper_2306_03336_b200.prng import fill_random_device
 
     nx, ny, steps, dtype, desc = WORKLOADS[args.workload]
+    if args.solve_steps:
+        steps = args.solve_steps
     tdt = torch.float64 if dtype == "f64" else torch.float32
     elem = 8 if dtype == "f64" else 4
     w = StencilWeights.diffusive(0.2)
@@ -464,16 +569,21 @@ def run_b200(args):
             raise RuntimeError("non-finite result")
 
     if rank != 0:
-        return
+        return None
     peaks = measured_peaks()
     kernel_s = total_ms * 1e-3 / args.steps
     cells_per_s = cells / kernel_s
     fp_peak = peaks["fp64_gops"] if elem == 8 else peaks["fp32_gops"]
+    # diffusive(0.2) has w == e == s == n: the kernels run the isotropic
+    # shared-product form, 2 products + 4 sums = 6 rounded ops per cell update
+    # (9 for general weights); the FP-pipe fraction counts the ops executed
+    ops = 6
     rooflines = {
         "smem": {"achieved": cells_per_s * 2 * elem / 1e9, "peak": peaks["smem_gbs"], "unit": "GB/s",
                  "bytes_per_cell": 2 * elem, "peak_src": "microbench LDS.128 (profiles/r01/microbench_peaks.log)"},
-        "fp_pipe": {"achieved": cells_per_s * 9 / 1e9, "peak": fp_peak, "unit": "Gop/s",
-                    "ops_per_cell": 9, "peak_src": "microbench DMUL/DADD (profiles/r01/microbench_peaks.log)"},
+        "fp_pipe": {"achieved": cells_per_s * ops / 1e9, "peak": fp_peak, "unit": "Gop/s",
+                    "ops_per_cell": ops, "ops_per_cell_general_weights": 9,
+                    "peak_src": "microbench DMUL/DADD (profiles/r01/microbench_peaks.log)"},
         "hbm": {"achieved": cells_per_s * 2 * elem / max(plan.halo, 1) / 1e9
                 if plan.mode in ("streaming", "pipe") else grid_bytes * 2 / kernel_s / 1e9,
                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "peak_src": peaks["hbm_src"]},
@@ -505,10 +615,11 @@ def run_b200(args):
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "e2e": e2e,
-        "cpu_baseline": cpu_reference_sample(min(nx, 1900), min(ny, 1900), dtype)
+        "cpu_baseline": cpu_reference_sample(min(nx, 1900), min(ny, 1900), dtype,
+                                             legs=not args.no_legs)
         if not args.no_cpu else None,
     }
-    print(json.dumps(line), flush=True)
+    return line
 
 
 def main():
@@ -519,10 +630,30 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-legs", action="store_true",
+                    help="cpu_baseline: only the all-core C port (skip the reference-structured legs)")
+    ap.add_argument("--no-c5", action="store_true", help="N=1: skip the C5 family anchors")
+    ap.add_argument("--no-strong", action="store_true", help="skip strong scaling at 32768^2")
     ap.add_argument("--solve-steps", type=int, default=0,
                     help="override the workload's Jacobi step count (quick runs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)  # the timing rules require >= 3 warm-up steps
+    if args.gpus < 1:
+        ap.error("--gpus must be at least 1")
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        # no launcher: one rank per GPU under torch.distributed.run
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        raise SystemExit(subprocess.call(cmd))
+    if world is not None and int(world) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started "
+                         f"WORLD_SIZE={world} ranks")
     if args.impl == "reference":
         run_reference(args)
     else:

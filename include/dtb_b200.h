@@ -164,6 +164,43 @@ int dtb_fill_random_rows_f64(double* d_out, int64_t nx, int64_t ny, int64_t pitc
                              uint64_t seed, double ghost, int64_t row0, int64_t nrows,
                              void* stream);
 
+/* ---- one process per GPU (multi-process y-slabs, fused halo exchange) ----
+ * A slab solver in process r keeps its padded local grid in two buffers
+ * allocated with dtb_ipc_malloc and shares their handles with its y-neighbour
+ * processes, which map them with dtb_ipc_open. Each epoch's solve then stores
+ * the rows the neighbours need straight into the neighbours' buffers from
+ * inside the pipelined kernel (NVLink P2P stores between GPUs), and restricts
+ * its own stores to the rows it owns: */
+typedef struct dtb_halo_mirror {
+  void* peer[2];          /* neighbour buffers (this process's mappings), or NULL */
+  int64_t r0[2], r1[2];   /* local padded rows [r0, r1) of the result go to peer i ... */
+  int64_t p0[2];          /* ... at its rows p0[i] .. (same pitch and column origin) */
+  int64_t sw0, sw1;       /* own stores only into local padded rows [sw0, sw1) */
+} dtb_halo_mirror;
+
+/* dtb_j2d5pt_*_dev with the fused halo stores of `mir` (the pipelined kernel
+ * runs the solve; its last pass writes the mirror rows). total_steps must not
+ * exceed the slab's halo depth; the caller orders epochs across processes
+ * (dtb_ipc_event_* below). */
+int dtb_j2d5pt_f64_dev_mirror(const double* d_in, double* d_out, int64_t nx, int64_t ny,
+                              int64_t pitch, const double w[5], int64_t total_steps,
+                              const dtb_halo_mirror* mir, void* stream, dtb_report* rep);
+int dtb_j2d5pt_f32_dev_mirror(const float* d_in, float* d_out, int64_t nx, int64_t ny,
+                              int64_t pitch, const float w[5], int64_t total_steps,
+                              const dtb_halo_mirror* mir, void* stream, dtb_report* rep);
+
+/* CUDA IPC: device buffers (cudaMalloc + cudaIpcGetMemHandle) and
+ * interprocess events; handles are 64 opaque bytes. */
+int dtb_ipc_malloc(int64_t bytes, void** ptr, uint8_t handle[64]);
+int dtb_ipc_free(void* ptr);
+int dtb_ipc_open(const uint8_t handle[64], void** ptr);
+int dtb_ipc_close(void* ptr);
+int dtb_ipc_event_create(void** event, uint8_t handle[64]);
+int dtb_ipc_event_open(const uint8_t handle[64], void** event);
+int dtb_event_destroy(void* event);
+int dtb_event_record(void* event, void* stream);
+int dtb_stream_wait_event(void* stream, void* event);
+
 /* Last error message on this thread ("" if none). */
 const char* dtb_last_error(void);
 

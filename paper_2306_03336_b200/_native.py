@@ -70,6 +70,14 @@ class DtbPlanInfo(ctypes.Structure):
     ]
 
 
+class DtbHaloMirror(ctypes.Structure):
+    _fields_ = [("peer", c_void_p * 2), ("r0", c_int64 * 2), ("r1", c_int64 * 2),
+                ("p0", c_int64 * 2), ("sw0", c_int64), ("sw1", c_int64)]
+
+
+IpcHandle = ctypes.c_uint8 * 64
+
+
 # every symbol include/dtb_b200.h declares, with its ctypes signature
 _SIGNATURES = {
     "dtb_j2d5pt_f64": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, POINTER(c_double),
@@ -98,6 +106,21 @@ _SIGNATURES = {
     "dtb_fill_random_rows_f64": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_uint64, c_double,
                                          c_int64, c_int64, c_void_p]),
     "dtb_last_error": (c_char_p, []),
+    "dtb_j2d5pt_f64_dev_mirror": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64,
+                                          POINTER(c_double), c_int64, POINTER(DtbHaloMirror),
+                                          c_void_p, POINTER(DtbReport)]),
+    "dtb_j2d5pt_f32_dev_mirror": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64,
+                                          POINTER(c_float), c_int64, POINTER(DtbHaloMirror),
+                                          c_void_p, POINTER(DtbReport)]),
+    "dtb_ipc_malloc": (c_int, [c_int64, POINTER(c_void_p), IpcHandle]),
+    "dtb_ipc_free": (c_int, [c_void_p]),
+    "dtb_ipc_open": (c_int, [IpcHandle, POINTER(c_void_p)]),
+    "dtb_ipc_close": (c_int, [c_void_p]),
+    "dtb_ipc_event_create": (c_int, [POINTER(c_void_p), IpcHandle]),
+    "dtb_ipc_event_open": (c_int, [IpcHandle, POINTER(c_void_p)]),
+    "dtb_event_destroy": (c_int, [c_void_p]),
+    "dtb_event_record": (c_int, [c_void_p, c_void_p]),
+    "dtb_stream_wait_event": (c_int, [c_void_p, c_void_p]),
     "dtb_debug_pipe_probe": (c_int, [POINTER(c_uint64)]),
 }
 

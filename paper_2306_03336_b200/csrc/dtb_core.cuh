@@ -48,8 +48,16 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
+// Steady rows per unrolled block of the band sweep and the epoch release
+// mode, per element type (B200 A/B on C2 / C3a: fp64 +1.8 % with 8-row blocks
+// and +2 % with one CTA-level release; fp32 -1 % / -2 % with either)
 #ifndef DTB_SWEEP_UNROLL
-#define DTB_SWEEP_UNROLL 4  // steady rows per unrolled block of the band sweep
+#define DTB_SWEEP_UNROLL(T) (sizeof(T) == 8 ? 8 : 4)
+#endif
+#ifndef DTB_PUB_CTA
+#define DTB_PUB_CTA(T) (sizeof(T) == 8)
 #endif
 
 namespace dtb {
@@ -316,10 +324,14 @@ struct Publisher {
   __device__ __forceinline__ void put_sides(const LaneAddr<T, K>& la, int r0, int r1) const {
     typedef Tile<T, K> L;
     const int w = wl + wr, n = (r1 - r0) * w;
+    if (w <= 0 || n <= 0) return;
     const int lane = threadIdx.x & 31;
-#pragma unroll 2
+    // element i = lane + 32 t of the (row, side column) list: (q, j) advance
+    // incrementally (one division per call, none per element)
+    const int dq = 32 / w, dj = 32 - dq * w;
+    int q = lane / w, j = lane - q * w;
     for (int i = lane; i < n; i += 32) {
-      const int q = i / w, j = i - q * w, r = r0 + q;
+      const int r = r0 + q;
       const int c = j < wl ? cl0 + j : cr0 + (j - wl);
       T v;
       if constexpr (sizeof(T) == 8) {
@@ -328,6 +340,12 @@ struct Publisher {
         asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(la.base + (uint32_t)(L::at(r, c) * 4)));
       }
       st_cg(g0 + (int64_t)r * pitch + c, v);
+      q += dq;
+      j += dj;
+      if (j >= w) {
+        j -= w;
+        ++q;
+      }
     }
   }
   __device__ __forceinline__ void put_rows(const LaneAddr<T, K>& la, int r0, int r1) const {
@@ -426,9 +444,10 @@ __device__ __forceinline__ void sweep2(const LaneAddr<T, K>& la, int Lh, int ya,
     store_row_at<CH>(rowp - 2 * RB, la.off, o);                   \
     rowp += RB;                                                   \
   }
-  for (; r + DTB_SWEEP_UNROLL < yb; r += DTB_SWEEP_UNROLL) {
+  constexpr int U = DTB_SWEEP_UNROLL(T);
+  for (; r + U < yb; r += U) {
 #pragma unroll
-    for (int u = 0; u < DTB_SWEEP_UNROLL / 2; ++u) {
+    for (int u = 0; u < U / 2; ++u) {
       DTB_SWEEP_ROW(x, y)
       DTB_SWEEP_ROW(y, x)
     }
@@ -498,8 +517,10 @@ __device__ __forceinline__ void band_rows(int Lh, int nb, int b, int& ya, int& y
 
 // Advance the tile `steps` time steps in place. All threads of the CTA call.
 // With `pub` non-null each warp publishes its band right after its own last
-// sweep and bumps the CTA's epoch flag with a release-add (neighbours wait
-// for nwarps bumps per epoch; no CTA barrier before the publish).
+// sweep; the CTA's epoch flag then goes up by nwarps — one release-add per
+// warp, or (DTB_PUB_CTA) one by thread 0 after the sweep's closing barrier,
+// whose fence is cumulative over the other warps' stores (PTX memory model:
+// bar.sync orders them before thread 0's release).
 template <typename T, int K, bool SYM, bool DYN>
 __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
                              const Weights<T>& wt, const Publisher<T, K>* pub = nullptr) {
@@ -513,11 +534,20 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
   lc.last_e = (Lw - 1) % K;
   const int rows = Lh - 2;
   if (rows <= 0 || Lw <= 2) return;
-  auto publish = [&](bool act, int ya, int yb) {
+  constexpr bool kPubCta = DTB_PUB_CTA(T);
+  auto publish = [&](bool act, int ya, int yb) {  // (followed by the sweep's barrier)
     if (act) pub->put_band(la, ya, yb);
-    __syncwarp();
-    if (lc.lane == 0)
-      asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
+    if (!kPubCta) {
+      __syncwarp();
+      if (lc.lane == 0)
+        asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
+    }
+  };
+  auto release_cta = [&]() {  // after the barrier that closes the publishing sweep
+    if (kPubCta && threadIdx.x == 0) {
+      __threadfence();
+      asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(pub->flag), "r"(nw) : "memory");
+    }
   };
   int s = 0;
   if (steps >= 2 && rows >= 2) {
@@ -529,6 +559,7 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
       sweep2<T, K, SYM, DYN>(la, Lh, ya, yb, act, wt, lc);
       if (pub && s + 2 == steps) publish(act, ya, yb);  // rows final: publish now
       __syncthreads();
+      if (pub && s + 2 == steps) release_cta();
     }
   }
   if (s < steps) {
@@ -540,6 +571,7 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
       sweep1<T, K, SYM, DYN>(la, Lh, ya, yb, act, wt, lc);
       if (pub && s + 1 == steps) publish(act, ya, yb);
       __syncthreads();
+      if (pub && s + 1 == steps) release_cta();
     }
   }
 }

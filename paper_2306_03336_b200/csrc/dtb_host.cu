@@ -618,6 +618,33 @@ void reset_call_state() {
   g_min_bytes = 0;
 }
 
+// one epoch of a multi-process slab with the fused halo stores (HaloMirror)
+template <typename T>
+int solve_dev_mirror(const T* d_in, T* d_out, int64_t nx, int64_t ny, int64_t pitch,
+                     const T w[5], int64_t total_steps, const dtb_halo_mirror* mir,
+                     cudaStream_t st, dtb_report* rep) {
+  if (!mir) return fail(DTB_EINVAL, "null halo mirror");
+  HaloMirror<T> m;
+  for (int i = 0; i < 2; ++i) {
+    m.peer[i] = static_cast<T*>(mir->peer[i]);
+    m.r0[i] = mir->r0[i];
+    m.r1[i] = mir->r1[i];
+    m.p0[i] = mir->p0[i];
+    if (m.peer[i] && (m.r0[i] < 0 || m.r1[i] > ny + 2 || m.r0[i] > m.r1[i] || m.p0[i] < 0))
+      return fail(DTB_ERANGE, "halo mirror %d rows [%lld, %lld) -> %lld outside the grid", i,
+                  (long long)m.r0[i], (long long)m.r1[i], (long long)m.p0[i]);
+    if (!m.peer[i]) m.r0[i] = m.r1[i] = 0;
+  }
+  m.sw0 = mir->sw0;
+  m.sw1 = mir->sw1;
+  struct MirrorScope {
+    explicit MirrorScope(const void* p) { g_halo_mirror = p; }
+    ~MirrorScope() { g_halo_mirror = nullptr; }
+  } scope(&m);
+  return solve_dev<T>(d_in, d_out, nx, ny, pitch, w, total_steps, 1, nullptr,
+                      DTB_FLAG_FORCE_PIPE, st, rep);
+}
+
 }  // namespace
 
 extern "C" {
@@ -700,6 +727,106 @@ int dtb_plan(int64_t nx, int64_t ny, int32_t elem_bytes, int64_t total_steps, in
   }
   out->computed_cells_per_step = p.computed_cells_per_step;
   out->est_cells_per_clk = p.cells_per_clk;
+  return DTB_OK;
+}
+
+int dtb_j2d5pt_f64_dev_mirror(const double* d_in, double* d_out, int64_t nx, int64_t ny,
+                              int64_t pitch, const double w[5], int64_t total_steps,
+                              const dtb_halo_mirror* mir, void* stream, dtb_report* rep) {
+  reset_call_state();
+  return solve_dev_mirror<double>(d_in, d_out, nx, ny, pitch, w, total_steps, mir,
+                                  (cudaStream_t)stream, rep);
+}
+
+int dtb_j2d5pt_f32_dev_mirror(const float* d_in, float* d_out, int64_t nx, int64_t ny,
+                              int64_t pitch, const float w[5], int64_t total_steps,
+                              const dtb_halo_mirror* mir, void* stream, dtb_report* rep) {
+  reset_call_state();
+  return solve_dev_mirror<float>(d_in, d_out, nx, ny, pitch, w, total_steps, mir,
+                                 (cudaStream_t)stream, rep);
+}
+
+int dtb_ipc_malloc(int64_t bytes, void** ptr, uint8_t handle[64]) {
+  reset_call_state();
+  if (!ptr || !handle || bytes < 1) return fail(DTB_EINVAL, "bad ipc allocation request");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  void* p = nullptr;
+  CUDA_TRY(cudaMalloc(&p, (size_t)bytes));
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    CUDA_TRY(e);
+  }
+  memcpy(handle, &h, 64);
+  *ptr = p;
+  return DTB_OK;
+}
+
+int dtb_ipc_free(void* ptr) {
+  reset_call_state();
+  CUDA_TRY(cudaFree(ptr));
+  return DTB_OK;
+}
+
+int dtb_ipc_open(const uint8_t handle[64], void** ptr) {
+  reset_call_state();
+  if (!ptr || !handle) return fail(DTB_EINVAL, "null ipc handle");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, 64);
+  CUDA_TRY(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return DTB_OK;
+}
+
+int dtb_ipc_close(void* ptr) {
+  reset_call_state();
+  CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+  return DTB_OK;
+}
+
+int dtb_ipc_event_create(void** event, uint8_t handle[64]) {
+  reset_call_state();
+  if (!event || !handle) return fail(DTB_EINVAL, "null event output");
+  static_assert(sizeof(cudaIpcEventHandle_t) == 64, "IPC event handle size");
+  cudaEvent_t ev;
+  CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventInterprocess));
+  cudaIpcEventHandle_t h;
+  const cudaError_t e = cudaIpcGetEventHandle(&h, ev);
+  if (e != cudaSuccess) {
+    cudaEventDestroy(ev);
+    CUDA_TRY(e);
+  }
+  memcpy(handle, &h, 64);
+  *event = ev;
+  return DTB_OK;
+}
+
+int dtb_ipc_event_open(const uint8_t handle[64], void** event) {
+  reset_call_state();
+  if (!event || !handle) return fail(DTB_EINVAL, "null event handle");
+  cudaIpcEventHandle_t h;
+  memcpy(&h, handle, 64);
+  cudaEvent_t ev;
+  CUDA_TRY(cudaIpcOpenEventHandle(&ev, h));
+  *event = ev;
+  return DTB_OK;
+}
+
+int dtb_event_destroy(void* event) {
+  reset_call_state();
+  CUDA_TRY(cudaEventDestroy((cudaEvent_t)event));
+  return DTB_OK;
+}
+
+int dtb_event_record(void* event, void* stream) {
+  reset_call_state();
+  CUDA_TRY(cudaEventRecord((cudaEvent_t)event, (cudaStream_t)stream));
+  return DTB_OK;
+}
+
+int dtb_stream_wait_event(void* stream, void* event) {
+  reset_call_state();
+  CUDA_TRY(cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)event, 0));
   return DTB_OK;
 }
 

@@ -458,6 +458,9 @@ pipe_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int n
                                     ctl[p].prod, ctl[p].cons, wt, lc, &mir);
     seq += pt.Lh;
   }
+  // mirror passes store into peer GPUs' (or other processes') buffers: make
+  // them system-visible before the kernel's completion is signalled
+  if (MIR) __threadfence_system();
 }
 
 template <typename T, int K, bool SYM, bool DYN>

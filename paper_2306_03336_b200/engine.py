@@ -144,7 +144,7 @@ def run_dtb(grid, weights, total_steps: int, plan=None, cfg: KernelConfig = Kern
     flags = _native.FLAG_POISON if poison else 0
     out, rep = _solve_host(grid.data, grid.nx, grid.ny, weights, total_steps, t_depth, valid,
                            ilp, flags, dtype)
-    result = Grid2D(grid.nx, grid.ny, out.astype(np.float64))
+    result = Grid2D(grid.nx, grid.ny, out.astype(np.float64, copy=False))
     if plan is not None:
         return result, model_dtb_traffic(plan, total_steps, valid)
     return result, _report(rep)
@@ -163,7 +163,7 @@ def run_dtb_b200(grid, weights, total_steps: int, *, valid=None, poison: bool = 
     out, rep = _solve_host(grid.data, grid.nx, grid.ny, weights, total_steps,
                            depth if depth is not None else 1, valid, 1,
                            flags | (_native.FLAG_POISON if poison else 0), dtype, n_gpus)
-    return Grid2D(grid.nx, grid.ny, out.astype(np.float64)), _report(rep)
+    return Grid2D(grid.nx, grid.ny, out.astype(np.float64, copy=False)), _report(rep)
 
 
 def j2d5pt(grid, weights, steps: int, *, dtype=np.float64) -> Grid2D:
@@ -174,7 +174,7 @@ def j2d5pt(grid, weights, steps: int, *, dtype=np.float64) -> Grid2D:
     if steps == 0:
         return Grid2D(grid.nx, grid.ny, np.array(grid.data, dtype=np.float64, copy=True))
     out, _ = _solve_host(grid.data, grid.nx, grid.ny, weights, steps, 1, None, 1, 0, dtype)
-    return Grid2D(grid.nx, grid.ny, out.astype(np.float64))
+    return Grid2D(grid.nx, grid.ny, out.astype(np.float64, copy=False))
 
 
 jacobi = j2d5pt

@@ -19,14 +19,25 @@ Results are bitwise identical to the single-GPU solve and to
 jacobi_reference for any world size (the inter-device analogue of the
 worker-count independence the reference tests, test_engine.py:61-77).
 
-The exchange backend is pluggable: torch.distributed point-to-point
-(NCCL over NVLink between GPUs; gloo for CPU tests) or in-process virtual
-ranks (several slabs on one device, used to check the decomposition on a
-single GPU without ranks that wait on each other).
+The exchange backend is pluggable:
+
+* ``"ipc"`` (fused, the default for CUDA ranks): each rank's two slab
+  buffers are CUDA IPC allocations whose handles the y-neighbours map; the
+  last pass of every epoch's pipelined kernel stores the rank's edge rows
+  straight into the neighbours' next-epoch buffers (NVLink P2P stores between
+  GPUs, dtb_j2d5pt_*_dev_mirror), so there is no separate exchange step.
+  Epochs are ordered by interprocess events (stream waits, ranks on
+  different GPUs) or by a host barrier after each epoch (ranks sharing one
+  GPU: no GPU-side wait on another process's kernels);
+* ``"p2p"``: torch.distributed point-to-point after each epoch (NCCL over
+  NVLink between GPUs; gloo for CPU tests);
+* in-process virtual ranks (:class:`VirtualSlabs`: several slabs on one
+  device, used to check the decomposition on a single GPU).
 """
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 __all__ = ["slab_rows", "SlabGeometry", "SlabSolver", "VirtualSlabs"]
@@ -89,19 +100,141 @@ class SlabGeometry:
                 raise ValueError(f"slab of {y1 - y0} rows is thinner than depth {self.depth}")
 
 
-class SlabSolver:
-    """One rank's slab. `backend` is torch.distributed (already initialised)
-    or None for a single rank; `local_solve(src, dst, nx, ny, steps)` advances
-    a padded local grid (the B200 kernel on GPU ranks)."""
+class _CudaArray:
+    """__cuda_array_interface__ view of a library-owned device allocation."""
 
-    def __init__(self, geo: SlabGeometry, local_solve, dist=None, group=None):
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 2, "strides": None}
+
+
+class _IpcLink:
+    """CUDA IPC plumbing of one rank (C ABI dtb_ipc_*): its two slab buffers
+    and two epoch events (parity), and its y-neighbours' mappings of theirs."""
+
+    def __init__(self, geo, pitch, torch_dtype, device, dist, group):
+        import torch
+        from . import _native
+        lib = _native.lib()
+        self.lib, self.geo, self.dist, self.group = lib, geo, dist, group
+        self.elem = torch.empty((), dtype=torch_dtype).element_size()
+        nbytes = (geo.local_ny + 2) * pitch * self.elem
+        self.bufs, self.events, self.opened, self.opened_events = [], [], [], []
+        handles = {"mem": [], "ev": []}
+        with torch.cuda.device(device):
+            for _ in range(2):
+                ptr, h = ctypes.c_void_p(), _native.IpcHandle()
+                if lib.dtb_ipc_malloc(nbytes, ctypes.byref(ptr), h) != 0:
+                    raise RuntimeError(_native.last_error())
+                self.bufs.append(ptr.value)
+                handles["mem"].append(bytes(h))
+                ev, eh = ctypes.c_void_p(), _native.IpcHandle()
+                if lib.dtb_ipc_event_create(ctypes.byref(ev), eh) != 0:
+                    raise RuntimeError(_native.last_error())
+                self.events.append(ev.value)
+                handles["ev"].append(bytes(eh))
+            typestr = "<f8" if self.elem == 8 else "<f4"
+            self._views = [_CudaArray(p, (geo.local_ny + 2, pitch), typestr) for p in self.bufs]
+            self.tensors = [torch.as_tensor(v, device=device) for v in self._views]
+            everyone = [None] * geo.world
+            dist.all_gather_object(everyone, (device.index, handles), group=group)
+            self.devices = [d for d, _ in everyone]
+            self.peer = {}  # rank -> ([buf0, buf1], [ev0, ev1])
+            for r in (geo.rank - 1, geo.rank + 1):
+                if 0 <= r < geo.world:
+                    _, hh = everyone[r]
+                    bufs, evs = [], []
+                    for hm, he in zip(hh["mem"], hh["ev"]):
+                        p, e = ctypes.c_void_p(), ctypes.c_void_p()
+                        if lib.dtb_ipc_open(_native.IpcHandle(*hm), ctypes.byref(p)) != 0:
+                            raise RuntimeError(_native.last_error())
+                        if lib.dtb_ipc_event_open(_native.IpcHandle(*he), ctypes.byref(e)) != 0:
+                            raise RuntimeError(_native.last_error())
+                        bufs.append(p.value)
+                        evs.append(e.value)
+                        self.opened.append(p.value)
+                        self.opened_events.append(e.value)
+                    self.peer[r] = (bufs, evs)
+        # ranks sharing one GPU are ordered by the host, never by a GPU wait
+        # on another process's work (B200 guide: no cross-process waits on one GPU)
+        self.host_sync = len(set(self.devices)) < len(self.devices)
+
+    def close(self):
+        for p in self.opened:
+            self.lib.dtb_ipc_close(ctypes.c_void_p(p))
+        for e in self.opened_events + self.events:
+            self.lib.dtb_event_destroy(ctypes.c_void_p(e))
+        self.tensors, self._views = [], []
+        for p in self.bufs:
+            self.lib.dtb_ipc_free(ctypes.c_void_p(p))
+        self.opened, self.opened_events, self.events, self.bufs = [], [], [], []
+
+
+class SlabSolver:
+    """One rank's slab. `dist` is torch.distributed (already initialised) or
+    None for a single rank; `local_solve(src, dst, nx, ny, steps)` advances a
+    padded local grid (the B200 kernel on GPU ranks). `exchange`: "ipc"
+    (fused halo stores, needs `weights`), "p2p" (torch.distributed
+    point-to-point after each epoch) or "auto" (ipc when it can be set up on
+    CUDA ranks, else p2p)."""
+
+    def __init__(self, geo: SlabGeometry, local_solve, dist=None, group=None,
+                 exchange: str = "p2p", weights=None):
         geo.validate()
+        if exchange not in ("auto", "ipc", "p2p"):
+            raise ValueError(f"unknown exchange mode {exchange!r}")
         self.geo = geo
         self.local_solve = local_solve
         self.dist = dist
         self.group = group
+        self.exchange_request = exchange
+        self.weights = weights
+        self.exchange_mode = "none" if geo.world == 1 else "p2p"
+        self.ipc = None
+        self.host_group = None
+        self.launches = 0
         self.a = None
         self.b = None
+
+    # -- local buffers -------------------------------------------------------
+    def allocate(self, pitch: int, torch_dtype, device):
+        """The two local buffers (local_ny+2, pitch). With exchange "ipc"/"auto"
+        and more than one rank they are CUDA IPC allocations mapped by the
+        neighbours (every rank must call this collectively)."""
+        import torch
+        g = self.geo
+        want_ipc = (g.world > 1 and self.exchange_request in ("ipc", "auto")
+                    and torch.device(device).type == "cuda")
+        if want_ipc:
+            if self.weights is None:
+                raise ValueError("the ipc exchange needs the stencil weights")
+            if self.host_group is None:
+                self.host_group = self.dist.new_group(backend="gloo")
+            err = None
+            try:
+                self.ipc = _IpcLink(g, pitch, torch_dtype, torch.device(device), self.dist,
+                                    self.host_group)
+            except Exception as e:  # noqa: BLE001 - agreed on below
+                err = e
+            oks = [None] * g.world
+            self.dist.all_gather_object(oks, err is None, group=self.host_group)
+            if all(oks):
+                self.exchange_mode = "ipc"
+                self.a, self.b = self.ipc.tensors
+                return self.a, self.b
+            if self.ipc is not None:
+                self.ipc.close()
+                self.ipc = None
+            if self.exchange_request == "ipc":
+                raise RuntimeError(f"ipc exchange unavailable: {err}")
+        self.a = torch.empty((g.local_ny + 2, pitch), dtype=torch_dtype, device=device)
+        self.b = torch.empty_like(self.a)
+        return self.a, self.b
+
+    def close(self):
+        if self.ipc is not None:
+            self.ipc.close()
+            self.ipc = None
 
     # -- local buffers -------------------------------------------------------
     def load(self, global_padded):
@@ -150,6 +283,8 @@ class SlabSolver:
         self.a, self.b = self.b, self.a
 
     def run(self, total_steps: int):
+        if self.exchange_mode == "ipc":
+            return self._run_ipc(total_steps)
         done = 0
         while done < total_steps:
             s = min(self.geo.depth, total_steps - done)
@@ -157,6 +292,72 @@ class SlabSolver:
             done += s
             if done < total_steps:
                 self.exchange()
+        return self
+
+    # -- fused exchange over CUDA IPC -----------------------------------------
+    def _mirror(self, out_idx: int):
+        """HaloMirror of one epoch: our first/last `depth` owned rows go into
+        the upper/lower neighbour's output buffer of this epoch, at its bottom
+        /top halo rows; our own stores stay inside our owned rows."""
+        from . import _native
+        g, ipc = self.geo, self.ipc
+        m = _native.DtbHaloMirror()
+        ht, own, d = g.halo_top, g.owned, g.depth
+        m.sw0 = 0 if g.rank == 0 else ht
+        m.sw1 = g.local_ny + 2 if g.rank == g.world - 1 else ht + own
+        if g.rank > 0:
+            up = SlabGeometry(g.nx, g.ny, g.world, g.rank - 1, d)
+            m.peer[0] = ipc.peer[g.rank - 1][0][out_idx]
+            m.r0[0], m.r1[0], m.p0[0] = ht, ht + d, up.halo_top + up.owned
+        if g.rank < g.world - 1:
+            m.peer[1] = ipc.peer[g.rank + 1][0][out_idx]
+            m.r0[1], m.r1[1], m.p0[1] = ht + own - d, ht + own, 0
+        return m
+
+    def _run_ipc(self, total_steps: int):
+        import torch
+        from . import _native
+        from .engine import _raise
+        g, ipc, lib = self.geo, self.ipc, self.ipc.lib
+        ptrs = [t.data_ptr() for t in ipc.tensors]
+        in_idx = ptrs.index(self.a.data_ptr())
+        pitch = self.a.stride(0)
+        f64 = self.a.dtype == torch.float64
+        fn = lib.dtb_j2d5pt_f64_dev_mirror if f64 else lib.dtb_j2d5pt_f32_dev_mirror
+        w = ((ctypes.c_double if f64 else ctypes.c_float) * 5)(*self.weights)
+        stream = torch.cuda.current_stream(self.a.device)
+        sp = ctypes.c_void_p(stream.cuda_stream)
+        nbrs = [r for r in (g.rank - 1, g.rank + 1) if r in ipc.peer]
+        rep = _native.DtbReport()
+        done, epoch = 0, 0
+        while done < total_steps:
+            s = min(g.depth, total_steps - done)
+            cur = epoch & 1
+            if epoch > 0 and not ipc.host_sync:
+                for r in nbrs:  # their previous epoch wrote our halo / read our target
+                    lib.dtb_stream_wait_event(sp, ctypes.c_void_p(ipc.peer[r][1][1 - cur]))
+            out_idx = 1 - in_idx
+            m = self._mirror(out_idx)
+            rc = fn(ptrs[in_idx], ptrs[out_idx], g.nx, g.local_ny, pitch, w, s, ctypes.byref(m),
+                    sp, ctypes.byref(rep))
+            if rc != _native.DTB_OK:
+                _raise(rc)
+            self.launches += int(lib.dtb_last_launch_count())
+            if ipc.host_sync:
+                stream.synchronize()
+            else:
+                lib.dtb_event_record(ctypes.c_void_p(ipc.events[cur]), sp)
+            # orders this record before the neighbours' waits on it (and their
+            # re-record of the same parity after their next wait)
+            self.dist.barrier(group=self.host_group)
+            in_idx = out_idx
+            done += s
+            epoch += 1
+        if not ipc.host_sync:  # no neighbour store into our buffers still in flight
+            for r in nbrs:
+                lib.dtb_stream_wait_event(sp, ctypes.c_void_p(ipc.peer[r][1][(epoch - 1) & 1]))
+            self.dist.barrier(group=self.host_group)
+        self.a, self.b = ipc.tensors[in_idx], ipc.tensors[1 - in_idx]
         return self
 
 

@@ -113,3 +113,31 @@ def test_prng_frozen_vectors(golden):
     assert [int(v) for v in splitmix64(1234567, 5)] == meta["prng"]["splitmix64_1234567"]
     assert random_interior(3, 2, 9).tolist() == meta["prng"]["random_interior_3x2_seed9"]
     assert np.array_equal(random_interior_c(30, 20, 77), random_interior(30, 20, 77))
+
+
+def test_reference_structured_ports_reproduce_reference_runs(golden):
+    """oracle/engine_port.py (the bench's BASELINE.md §4 CPU legs): the
+    row-wise jacobi_reference restatement and the DTB engine restatement
+    reproduce the reference's run_dtb outputs (tests/golden, no valid region)
+    and the C oracle, bit for bit."""
+    from oracle.engine_port import jacobi_rowwise, run_dtb_port
+    from paper_2306_03336_b200 import DeviceModel, StencilWeights, plan_device_tiles
+    meta, arr = golden
+    w = StencilWeights.diffusive(0.2).astuple()
+    checked = 0
+    for r in meta["runs"]:
+        if r["valid"] is not None:
+            continue
+        g = arr[f"{r['key']}_in"]
+        want = arr[f"{r['key']}_out"]
+        plan = plan_device_tiles((r["nx"], r["ny"]), DeviceModel("d", r["workers"], r["cap"]),
+                                 r["t_depth"])
+        for threads in (1, 3):
+            assert np.array_equal(bits(run_dtb_port(g, w, r["steps"], plan, threads)),
+                                  bits(want)), (r["key"], threads)
+        assert np.array_equal(bits(jacobi_rowwise(g, w, r["steps"])), bits(want)), r["key"]
+        checked += 1
+    assert checked >= 5
+    g = grid_new(67, 45, random_interior(67, 45, 3), ghost=0.5).data
+    mixed = (0.11, -0.2, 0.37, 0.5, -0.07)
+    assert np.array_equal(bits(jacobi_rowwise(g, mixed, 7)), bits(jacobi_c(g, mixed, 7)))
