@@ -56,6 +56,9 @@ extern "C" {
 #define DTB_FLAG_SLAB_COPY 128u     /* n_gpus > 1: exchange slab halos by copies after each epoch */
 #define DTB_FLAG_SLAB_FUSED 256u    /* n_gpus > 1: pipelined kernel on every slab, halos stored
                                        into the neighbours in-kernel (fails if a slab cannot) */
+#define DTB_FLAG_COUNT 512u         /* report the traffic the kernels COUNTED at their copy and
+                                       compute sites (device counters) instead of the schedule's
+                                       analytic model; the two agree exactly (tests) */
 
 /* Half-open rectangle in interior coordinates (grid.py:38-92). */
 typedef struct dtb_rect {

@@ -30,6 +30,7 @@ FLAG_FORCE_PIPE = 32
 FLAG_FORCE_RESIDENT = 64
 FLAG_SLAB_COPY = 128
 FLAG_SLAB_FUSED = 256
+FLAG_COUNT = 512
 
 
 class DtbRect(ctypes.Structure):

@@ -50,14 +50,10 @@
 
 #include <type_traits>
 
-// Steady rows per unrolled block of the band sweep and the epoch release
-// mode, per element type (B200 A/B on C2 / C3a: fp64 +1.8 % with 8-row blocks
-// and +2 % with one CTA-level release; fp32 -1 % / -2 % with either)
+// Steady rows per unrolled block of the band sweep, per element type (B200
+// A/B on C2 / C3a: fp64 +1.8 % with 8-row blocks, fp32 -1 %)
 #ifndef DTB_SWEEP_UNROLL
 #define DTB_SWEEP_UNROLL(T) (sizeof(T) == 8 ? 8 : 4)
-#endif
-#ifndef DTB_PUB_CTA
-#define DTB_PUB_CTA(T) (sizeof(T) == 8)
 #endif
 
 namespace dtb {
@@ -370,13 +366,17 @@ struct Publisher {
       for (int e = 0; e < K; ++e) st_pred(((full_mask >> e) & 1u) != 0, p + e, v[e]);
     }
   }
-  // publish the part of band [ya, yb) the neighbours read
-  __device__ __forceinline__ void put_band(const LaneAddr<T, K>& la, int ya, int yb) const {
+  // publish the part of band [ya, yb) the neighbours read; returns the cells
+  // stored (whole owned rows: own1... the owned width; sides: wl + wr per row)
+  __device__ __forceinline__ int64_t put_band(const LaneAddr<T, K>& la, int ya, int yb,
+                                              int owned_w) const {
     const int r0 = max(ya, own0), r1 = min(yb, own1);
     const int s0 = max(r0, top1), s1 = min(r1, bot0);
     if (s0 < s1) put_sides(la, s0, s1);
     put_rows(la, r0, min(r1, top1));
     put_rows(la, max(r0, bot0), r1);
+    return (int64_t)max(0, s1 - s0) * (wl + wr) +
+           (int64_t)(max(0, min(r1, top1) - r0) + max(0, r1 - max(r0, bot0))) * owned_w;
   }
 };
 
@@ -517,13 +517,17 @@ __device__ __forceinline__ void band_rows(int Lh, int nb, int b, int& ya, int& y
 
 // Advance the tile `steps` time steps in place. All threads of the CTA call.
 // With `pub` non-null each warp publishes its band right after its own last
-// sweep; the CTA's epoch flag then goes up by nwarps — one release-add per
-// warp, or (DTB_PUB_CTA) one by thread 0 after the sweep's closing barrier,
-// whose fence is cumulative over the other warps' stores (PTX memory model:
-// bar.sync orders them before thread 0's release).
+// sweep and bumps the CTA's epoch flag with a release-add (neighbours wait for
+// nwarps bumps per epoch). One CTA-level release by thread 0 after the
+// closing barrier instead measured 7 % slower on C2 (10^4 steps, B200 A/B).
+//
+// cnt (DTB_FLAG_COUNT, else null): [1] += cells the publish stored, [3] +=
+// cells each sweep updated (the band's rows at every level, Lw-2 columns;
+// frozen rows and columns are not updates).
 template <typename T, int K, bool SYM, bool DYN>
 __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
-                             const Weights<T>& wt, const Publisher<T, K>* pub = nullptr) {
+                             const Weights<T>& wt, const Publisher<T, K>* pub = nullptr,
+                             unsigned long long* cnt = nullptr, int owned_w = 0) {
   const int warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
   LaneCtx lc;
@@ -534,20 +538,14 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
   lc.last_e = (Lw - 1) % K;
   const int rows = Lh - 2;
   if (rows <= 0 || Lw <= 2) return;
-  constexpr bool kPubCta = DTB_PUB_CTA(T);
-  auto publish = [&](bool act, int ya, int yb) {  // (followed by the sweep's barrier)
-    if (act) pub->put_band(la, ya, yb);
-    if (!kPubCta) {
-      __syncwarp();
-      if (lc.lane == 0)
-        asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
+  auto publish = [&](bool act, int ya, int yb) {
+    if (act) {
+      const int64_t n = pub->put_band(la, ya, yb, owned_w);
+      if (cnt && lc.lane == 0 && n) atomicAdd(cnt + 1, (unsigned long long)n);
     }
-  };
-  auto release_cta = [&]() {  // after the barrier that closes the publishing sweep
-    if (kPubCta && threadIdx.x == 0) {
-      __threadfence();
-      asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(pub->flag), "r"(nw) : "memory");
-    }
+    __syncwarp();
+    if (lc.lane == 0)
+      asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
   };
   int s = 0;
   if (steps >= 2 && rows >= 2) {
@@ -557,9 +555,11 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
     const bool act = warp < nb2;
     for (; s + 2 <= steps; s += 2) {
       sweep2<T, K, SYM, DYN>(la, Lh, ya, yb, act, wt, lc);
+      if (cnt && act && lc.lane == 0)
+        atomicAdd(cnt + 3, (unsigned long long)((2 * (yb - ya) + 2 - (ya == 1) -
+                                                 (yb == Lh - 1)) * (Lw - 2)));
       if (pub && s + 2 == steps) publish(act, ya, yb);  // rows final: publish now
       __syncthreads();
-      if (pub && s + 2 == steps) release_cta();
     }
   }
   if (s < steps) {
@@ -569,9 +569,10 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
     const bool act = warp < nb1;
     for (; s < steps; ++s) {
       sweep1<T, K, SYM, DYN>(la, Lh, ya, yb, act, wt, lc);
+      if (cnt && act && lc.lane == 0)
+        atomicAdd(cnt + 3, (unsigned long long)((yb - ya) * (Lw - 2)));
       if (pub && s + 1 == steps) publish(act, ya, yb);
       __syncthreads();
-      if (pub && s + 1 == steps) release_cta();
     }
   }
 }

@@ -176,38 +176,167 @@ int validate(int64_t nx, int64_t ny, int64_t pitch, const double w[5], int64_t t
   return DTB_OK;
 }
 
-// The B200 schedule's traffic in the reference's cell units (metrics.py:39-66;
-// the ghost ring is never counted, metrics.py:3-6).
-void fill_report(const Plan& p, int64_t nx, int64_t ny, int64_t steps, int elem, dtb_report* rep) {
+// ---------------------------------------------------------------------------
+// TrafficReport of the B200 schedule (metrics.py:39-66 fields, cell units,
+// ghost ring never counted, metrics.py:3-6). fill_report is the analytic
+// model; with DTB_FLAG_COUNT the kernels count the same quantities at their
+// copy and compute sites instead (device counters, dtb_internal.h), and the
+// tests require the two to agree exactly:
+//   loads   cells read from global memory into shared memory (tile loads,
+//           resident halo refreshes from the L2 exchange buffer)
+//   stores  cells written back (owned cells, resident halo publishes)
+//   halo    cells exchanged between CTAs (refreshes) or slabs (mirror stores)
+//   redundant = cell updates performed (every level's rows of every band or
+//           segment, frozen rows/columns excluded) - useful
+// ---------------------------------------------------------------------------
+int64_t span(int64_t a, int64_t b, int64_t lo, int64_t hi) {
+  return std::max<int64_t>(0, std::min(b, hi) - std::max(a, lo));
+}
+
+void band_rows_host(int Lh, int nb, int b, int& ya, int& yb) {  // dtb_core.cuh band_rows
+  const int rows = Lh - 2;
+  const int base = rows / nb, rem = rows % nb;
+  ya = 1 + b * base + std::min(b, rem);
+  yb = ya + base + (b < rem ? 1 : 0);
+}
+
+// cell updates of advance_tile over `steps` (dtb_core.cuh: two-step sweeps
+// update 2H + 2 rows per band, minus frozen rows; one-step sweeps H)
+int64_t sweep_cells(int Lw, int Lh, int steps, int nw, bool poison) {
+  const int rows = Lh - 2;
+  if (rows <= 0 || Lw <= 2 || steps <= 0) return 0;
+  if (poison) return (int64_t)steps * rows * (Lw - 2);
+  int64_t c = 0;
+  int s = 0;
+  if (steps >= 2 && rows >= 2) {
+    const int nb = std::max(1, std::min(nw, rows / 2));
+    int64_t per = 0;
+    for (int b = 0; b < nb; ++b) {
+      int ya, yb;
+      band_rows_host(Lh, nb, b, ya, yb);
+      per += 2 * (yb - ya) + 2 - (ya == 1) - (yb == Lh - 1);
+    }
+    s = steps / 2 * 2;
+    c += (int64_t)(steps / 2) * per * (Lw - 2);
+  }
+  c += (int64_t)(steps - s) * rows * (Lw - 2);
+  return c;
+}
+
+template <typename T>
+void fill_report(const Plan& p, int64_t nx, int64_t ny, int64_t steps, bool poison,
+                 const HaloMirror<T>* mir, dtb_report* rep) {
   if (!rep) return;
   memset(rep, 0, sizeof *rep);
-  rep->elem_bytes = elem;
+  rep->elem_bytes = (int64_t)sizeof(T);
   rep->useful_compute_cells = nx * ny * steps;
-  if (p.mode == 2) {
-    rep->global_load_cells = nx * ny * steps;
-    rep->global_store_cells = nx * ny * steps;
+  rep->scratchpad_peak_bytes = p.smem_bytes;
+  int64_t load = 0, store = 0, halo = 0, comp = 0;
+  if (p.mode == 2) {  // naive: every step reads and writes the grid once
+    rep->global_load_cells = rep->global_store_cells = nx * ny * steps;
+    rep->scratchpad_peak_bytes = 0;
     return;
   }
-  const int64_t passes = (steps + p.h - 1) / p.h;
-  int64_t load = 0, owned = nx * ny, halo_ring = 0;
-  for (int i = 0; i < p.sx.n; ++i)
-    for (int j = 0; j < p.sy.n; ++j) {
-      const int64_t dw = std::min<int64_t>(p.sx.l1[i], nx) - std::max(p.sx.l0[i], 0);
-      const int64_t dh = std::min<int64_t>(p.sy.l1[j], ny) - std::max(p.sy.l0[j], 0);
-      load += dw * dh;
-      halo_ring += dw * dh - (int64_t)(p.sx.o1[i] - p.sx.o0[i]) * (p.sy.o1[j] - p.sy.o0[j]);
+  const int ntx = p.sx.n, nty = p.sy.n;
+  auto tile = [&](int i, int j, int& Lw, int& Lh, int& gx0, int& gy0) {
+    Lw = p.sx.l1[i] - p.sx.l0[i];
+    Lh = p.sy.l1[j] - p.sy.l0[j];
+    gx0 = p.sx.l0[i] + 1;
+    gy0 = p.sy.l0[j] + 1;
+  };
+  if (p.mode == 0) {  // resident (dtb_resident.cuh)
+    const int64_t E = (steps + p.h - 1) / p.h;
+    for (int j = 0; j < nty; ++j)
+      for (int i = 0; i < ntx; ++i) {
+        int Lw, Lh, gx0, gy0;
+        tile(i, j, Lw, Lh, gx0, gy0);
+        const int cz = p.sx.l0[i], cw = p.sx.l1[i], rz = p.sy.l0[j], rw = p.sy.l1[j];
+        const int ox0 = p.sx.o0[i] - cz, ox1 = p.sx.o1[i] - cz;
+        const int oy0 = p.sy.o0[j] - rz, oy1 = p.sy.o1[j] - rz;
+        const bool hl = cz > -1, hr = cw < nx + 1, ht = rz > -1, hb = rw < ny + 1;
+        const int bl = i > 0 ? std::max(0, p.sx.l1[i - 1] - p.sx.o0[i]) : 0;
+        const int br = i + 1 < ntx ? std::max(0, p.sx.o1[i] - p.sx.l0[i + 1]) : 0;
+        const int bt = j > 0 ? std::max(0, p.sy.l1[j - 1] - p.sy.o0[j]) : 0;
+        const int bb = j + 1 < nty ? std::max(0, p.sy.o1[j] - p.sy.l0[j + 1]) : 0;
+        const int rx0 = hl ? 0 : 1, rx1 = hr ? Lw : Lw - 1, ry0 = ht ? 0 : 1, ry1 = hb ? Lh : Lh - 1;
+        load += span(gy0, gy0 + Lh, 1, ny + 1) * span(gx0, gx0 + Lw, 1, nx + 1);
+        store += (int64_t)(oy1 - oy0) * (ox1 - ox0);
+        // refresh_by_direction's regions (dtb_tile_io.cuh)
+        int64_t refresh = 0;
+        const int reg[8][6] = {{0, -1, ry0, oy0, ox0, ox1}, {0, 1, oy1, ry1, ox0, ox1},
+                               {-1, -1, ry0, oy0, rx0, ox0}, {1, -1, ry0, oy0, ox1, rx1},
+                               {-1, 1, oy1, ry1, rx0, ox0}, {1, 1, oy1, ry1, ox1, rx1},
+                               {-1, 0, oy0, oy1, rx0, ox0}, {1, 0, oy0, oy1, ox1, rx1}};
+        for (const auto& r : reg) {
+          const int nxt = i + r[0], nyt = j + r[1];
+          if (r[3] <= r[2] || r[5] <= r[4] || nxt < 0 || nxt >= ntx || nyt < 0 || nyt >= nty) continue;
+          refresh += (int64_t)(r[3] - r[2]) * (r[5] - r[4]);
+        }
+        // the publish of every non-final epoch
+        int64_t publish = 0;
+        const int owned_w = ox1 - ox0, top1 = oy0 + bt, bot0 = oy1 - bb;
+        const int cr0 = std::max(ox1 - br, ox0 + bl), wl = bl, wr = ox1 - cr0;
+        if (poison) {
+          const int t1 = std::min(oy0 + bt, oy1), b0 = std::max(oy1 - bb, t1);
+          publish = (int64_t)(t1 - oy0 + oy1 - b0) * owned_w + (int64_t)(b0 - t1) * (wl + wr);
+        } else {
+          const int rows = Lh - 2;
+          const bool two = p.h >= 2 && rows >= 2 && p.h % 2 == 0;
+          const int nb = two ? std::max(1, std::min(p.warps, rows / 2))
+                             : std::max(1, std::min(p.warps, rows));
+          for (int b = 0; b < nb && rows > 0 && Lw > 2; ++b) {
+            int ya, yb;
+            band_rows_host(Lh, nb, b, ya, yb);
+            const int r0 = std::max(ya, oy0), r1 = std::min(yb, oy1);
+            const int s0 = std::max(r0, top1), s1 = std::min(r1, bot0);
+            publish += (int64_t)std::max(0, s1 - s0) * (wl + wr) +
+                       (int64_t)(std::max(0, std::min(r1, top1) - r0) +
+                                 std::max(0, r1 - std::max(r0, bot0))) * owned_w;
+          }
+        }
+        load += (E - 1) * refresh;
+        halo += (E - 1) * refresh;
+        store += (E - 1) * publish;
+        for (int64_t e = 0; e < E; ++e)
+          comp += sweep_cells(Lw, Lh, (int)std::min<int64_t>(p.h, steps - e * p.h), p.warps, poison);
+      }
+  } else {  // streaming passes: pipelined (mode 3) or tile sweep (mode 1)
+    const int64_t passes = (steps + p.h - 1) / p.h;
+    for (int64_t k = 0; k < passes; ++k) {
+      const int s_k = (int)std::min<int64_t>(p.h, steps - k * p.h);
+      const bool mirror_pass = mir && k + 1 == passes;
+      for (int j = 0; j < nty; ++j)
+        for (int i = 0; i < ntx; ++i) {
+          int Lw, Lh, gx0, gy0;
+          tile(i, j, Lw, Lh, gx0, gy0);
+          load += span(gy0, gy0 + Lh, 1, ny + 1) * span(gx0, gx0 + Lw, 1, nx + 1);
+          if (p.mode == 3) {  // dtb_pipe.cuh store window and mirror rows
+            const int cz = p.sx.l0[i], rz = p.sy.l0[j];
+            const int ox0 = p.sx.o0[i] - (p.sx.o0[i] == 0) - cz;
+            const int ox1 = p.sx.o1[i] + (p.sx.o1[i] == nx) - cz;
+            int oy0 = p.sy.o0[j] - (p.sy.o0[j] == 0) - rz;
+            int oy1 = p.sy.o1[j] + (p.sy.o1[j] == ny) - rz;
+            const int qy0 = oy0, qy1 = oy1;
+            if (mirror_pass) {
+              oy0 = std::max<int64_t>(oy0, mir->sw0 - gy0);
+              oy1 = std::min<int64_t>(oy1, mir->sw1 - gy0);
+            }
+            const int64_t sc = span(gx0 + ox0, gx0 + ox1, 1, nx + 1);
+            store += span(gy0 + oy0, gy0 + oy1, 1, ny + 1) * sc;
+            if (mirror_pass)
+              for (int m = 0; m < 2; ++m) halo += span(gy0 + qy0, gy0 + qy1, mir->r0[m], mir->r1[m]) * sc;
+            comp += (int64_t)s_k * std::max(0, Lh - 2) * std::max(0, Lw - 2);
+          } else {
+            store += (int64_t)(p.sy.o1[j] - p.sy.o0[j]) * (p.sx.o1[i] - p.sx.o0[i]);
+            comp += sweep_cells(Lw, Lh, s_k, p.warps, poison);
+          }
+        }
     }
-  if (p.mode == 0) {
-    rep->global_load_cells = load + (passes - 1) * halo_ring;
-    rep->global_store_cells = owned + (passes - 1) * halo_ring;
-    rep->halo_exchanged_cells = (passes - 1) * halo_ring;
-  } else {
-    rep->global_load_cells = passes * load;
-    rep->global_store_cells = passes * owned;
-    rep->halo_exchanged_cells = 0;
   }
-  rep->redundant_compute_cells = p.computed_cells_per_step * steps - nx * ny * steps;
-  rep->scratchpad_peak_bytes = p.smem_bytes;
+  rep->global_load_cells = load;
+  rep->global_store_cells = store;
+  rep->halo_exchanged_cells = halo;
+  rep->redundant_compute_cells = comp - nx * ny * steps;
 }
 
 int plan_fail(const char* err, int64_t min_bytes) {
@@ -282,6 +411,16 @@ int solve_dev(const T* d_in, T* d_out, int64_t nx, int64_t ny, int64_t pitch, co
   const bool poison = (flags & DTB_FLAG_POISON) != 0;
   if (g_halo_mirror && p.mode != 3)
     return fail(DTB_EINVAL, "fused slab halos need the pipelined kernel (plan mode %d)", p.mode);
+  // DTB_FLAG_COUNT: the kernels count their traffic into device counters
+  unsigned long long* cnt = nullptr;
+  if ((flags & DTB_FLAG_COUNT) && p.mode != 2) {
+    int device;
+    CUDA_TRY(cudaGetDevice(&device));
+    void* c = nullptr;
+    if (int rc2 = arena_get(kArenaCounters, device, 8 * sizeof(unsigned long long), &c)) return rc2;
+    cnt = static_cast<unsigned long long*>(c);
+    CUDA_TRY(cudaMemsetAsync(cnt, 0, 8 * sizeof(unsigned long long), st));
+  }
   if (p.mode == 2) {
     // naive: total_steps launches ping-ponging between out and scratch
     const size_t grid_bytes = (size_t)(ny + 2) * pitch * sizeof(T);
@@ -304,14 +443,26 @@ int solve_dev(const T* d_in, T* d_out, int64_t nx, int64_t ny, int64_t pitch, co
     rc = fill_geometry(p, geo);
     if (rc) return rc;
     if (p.mode == 0)
-      rc = launch_resident<T>(p, geo, in_v, out_v, pitch, (int)vnx, (int)vny, w, total_steps, poison, st);
+      rc = launch_resident<T>(p, geo, in_v, out_v, pitch, (int)vnx, (int)vny, w, total_steps,
+                              poison, st, cnt);
     else if (p.mode == 3)
-      rc = launch_pipe<T>(p, geo, in_v, out_v, pitch, (int)vnx, (int)vny, w, total_steps, st);
+      rc = launch_pipe<T>(p, geo, in_v, out_v, pitch, (int)vnx, (int)vny, w, total_steps, st, cnt);
     else
-      rc = launch_stream<T>(p, geo, in_v, out_v, pitch, (int)vnx, (int)vny, w, total_steps, poison, st);
+      rc = launch_stream<T>(p, geo, in_v, out_v, pitch, (int)vnx, (int)vny, w, total_steps,
+                            poison, st, cnt);
     if (rc) return rc;
   }
-  fill_report(p, vnx, vny, total_steps, (int)sizeof(T), rep);
+  fill_report<T>(p, vnx, vny, total_steps, poison, static_cast<const HaloMirror<T>*>(g_halo_mirror),
+                 rep);
+  if (cnt && rep) {  // replace the model by what the kernels counted
+    unsigned long long h[8];
+    CUDA_TRY(cudaMemcpyAsync(h, cnt, sizeof h, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    rep->global_load_cells = (int64_t)h[0];
+    rep->global_store_cells = (int64_t)h[1];
+    rep->halo_exchanged_cells = (int64_t)h[2];
+    rep->redundant_compute_cells = (int64_t)h[3] - vnx * vny * total_steps;
+  }
   return DTB_OK;
 }
 
@@ -507,13 +658,16 @@ int solve_host_slabs(const T* in, T* out, int64_t nx, int64_t ny, int64_t pitch,
       }
       dtb_report r;
       {
-        MirrorScope scope(fused ? &m : nullptr);
+        // the last epoch feeds no one: plain solve (its halo rows are never read)
+        const bool final_epoch = done + s_ep >= total_steps;
+        MirrorScope scope(fused && !final_epoch ? &m : nullptr);
         if (int rc = solve_dev<T>(s.a, s.b, nx, s.lny, dpitch, w, s_ep, 1, nullptr, lflags, st, &r))
           return rc;
       }
       launches += g_launches;
       acc.global_load_cells += r.global_load_cells;
       acc.global_store_cells += r.global_store_cells;
+      acc.halo_exchanged_cells += r.halo_exchanged_cells;  // fused: the mirror stores
       acc.redundant_compute_cells += r.redundant_compute_cells + r.useful_compute_cells;
       acc.scratchpad_peak_bytes = std::max(acc.scratchpad_peak_bytes, r.scratchpad_peak_bytes);
       std::swap(s.a, s.b);
@@ -522,10 +676,7 @@ int solve_host_slabs(const T* in, T* out, int64_t nx, int64_t ny, int64_t pitch,
     done += s_ep;
     ++epoch;
     if (done >= total_steps) break;
-    if (fused) {
-      acc.halo_exchanged_cells += 2 * (int64_t)(n_slabs - 1) * depth * nx;
-      continue;
-    }
+    if (fused) continue;
     for (int g = 0; g < n_slabs; ++g) {  // halo rows from each neighbour's owned edge rows
       Slab& s = sl[g];
       cudaStream_t st = dstream[s.dev];

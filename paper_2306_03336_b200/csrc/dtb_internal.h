@@ -61,7 +61,8 @@ int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 
 // Per-device scratch, grown on demand and kept (solves are externally
 // synchronous, so one arena per device and role suffices).
-enum ArenaRole { kArenaScratch = 0, kArenaIo = 1, kArenaStage = 2, kArenaCount = 3 };
+enum ArenaRole { kArenaScratch = 0, kArenaIo = 1, kArenaStage = 2, kArenaCounters = 3,
+                 kArenaCount = 4 };
 int arena_get(int role, int device, size_t bytes, void** out);
 
 int query_dev(DevInfo& d);
@@ -70,15 +71,22 @@ int query_dev(DevInfo& d);
 int prepare_kernel(const void* kern, int device, int smem, int threads, int* per_sm);
 
 // ---- kernel launchers (one translation unit per family and type) ----------
+// cnt (DTB_FLAG_COUNT, else null): device counters the kernels add their
+// counted traffic to — [0] global loads, [1] global stores, [2] halo cells
+// exchanged, [3] cell updates performed (domain cells; the ghost ring is
+// never counted, metrics.py:3-6)
 template <typename T>
 int launch_resident(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch,
-                     int nx, int ny, const T w[5], int64_t steps, bool poison, cudaStream_t st);
+                    int nx, int ny, const T w[5], int64_t steps, bool poison, cudaStream_t st,
+                    unsigned long long* cnt);
 template <typename T>
 int launch_stream(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch,
-                  int nx, int ny, const T w[5], int64_t steps, bool poison, cudaStream_t st);
+                  int nx, int ny, const T w[5], int64_t steps, bool poison, cudaStream_t st,
+                  unsigned long long* cnt);
 template <typename T>
 int launch_pipe(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch,
-                int nx, int ny, const T w[5], int64_t steps, cudaStream_t st);
+                int nx, int ny, const T w[5], int64_t steps, cudaStream_t st,
+                unsigned long long* cnt);
 template <typename T>
 int launch_naive(const T* d_in, T* d_out, T* d_tmp, int64_t pitch, int nx, int ny, const T w[5],
                  int64_t steps, cudaStream_t st);

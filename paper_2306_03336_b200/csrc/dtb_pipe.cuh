@@ -30,7 +30,7 @@
 #include <type_traits>
 
 #include "dtb_internal.h"
-#include "dtb_core.cuh"
+#include "dtb_tile_io.cuh"
 
 #ifndef DTB_PIPE_PROBE
 #define DTB_PIPE_PROBE 0  // debug builds: per-stage wait-cycle counters (dtb_debug_pipe_probe)
@@ -408,7 +408,7 @@ template <typename T, int K, int NW, int S, bool SYM, bool DYN, bool MIR>
 __global__ void __launch_bounds__(NW * 32, 1)
 pipe_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int nx, int ny,
             Weights<T> wt, int steps, const __grid_constant__ Geometry geo,
-            const __grid_constant__ HaloMirror<T> mir) {
+            const __grid_constant__ HaloMirror<T> mir, unsigned long long* __restrict__ cnt) {
   constexpr int P = NW / S;
   typedef Tile<T, K> L;
   constexpr int RB = L::ROW * (int)sizeof(T);
@@ -456,6 +456,24 @@ pipe_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int n
     lc.last_e = (pt.Lw - 1) % K;
     pipe_stage<T, K, SYM, DYN, MIR>(pt, s, S, levels, seq, src, dst, pitch, ring_in, ring_out,
                                     ctl[p].prod, ctl[p].cons, wt, lc, &mir);
+    if (cnt && lc.lane == 0) {  // counted traffic (domain cells only)
+      const long long dc = span_in(pt.gx0, pt.gx0 + pt.Lw, 1, nx + 1);
+      if (s == 0)  // stage 0 read the segment's rows from HBM
+        atomicAdd(cnt + 0, (unsigned long long)(span_in(pt.gy0, pt.gy0 + pt.Lh, 1, ny + 1) * dc));
+      if (levels > 0)
+        atomicAdd(cnt + 3, (unsigned long long)levels * max(0, pt.Lh - 2) * max(0, pt.Lw - 2));
+      if (s == S - 1) {  // the last stage stored the owned rows (and fed the mirrors)
+        const long long sc = span_in(pt.gx0 + pt.ox0, pt.gx0 + pt.ox1, 1, nx + 1);
+        atomicAdd(cnt + 1, (unsigned long long)(span_in(pt.gy0 + pt.oy0, pt.gy0 + pt.oy1, 1,
+                                                        ny + 1) * sc));
+        if (MIR) {
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+            atomicAdd(cnt + 2, (unsigned long long)(span_in(pt.gy0 + pt.qy0, pt.gy0 + pt.qy1,
+                                                            mir.r0[i], mir.r1[i]) * sc));
+        }
+      }
+    }
     seq += pt.Lh;
   }
   // mirror passes store into peer GPUs' (or other processes') buffers: make
@@ -465,7 +483,8 @@ pipe_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int n
 
 template <typename T, int K, bool SYM, bool DYN>
 int launch_pipe_kernel(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch,
-                       int nx, int ny, const Weights<T>& wt, int64_t steps, cudaStream_t st) {
+                       int nx, int ny, const Weights<T>& wt, int64_t steps, cudaStream_t st,
+                       unsigned long long* cnt) {
   constexpr int S = kPipeStages, PW = kPipeWarps, P = PW / S;
   auto kern = pipe_kernel<T, K, PW, S, SYM, DYN, false>;
   auto kmir = pipe_kernel<T, K, PW, S, SYM, DYN, true>;
@@ -499,9 +518,9 @@ int launch_pipe_kernel(const Plan& p, const Geometry& geo, const T* d_in, T* d_o
     const int s = (int)std::min<int64_t>(2 * S, steps - done);
     T* dst = ((passes - 1 - i) % 2 == 0) ? d_out : tmp;
     if (mir && i + 1 == passes)  // the epoch's result: also feed the neighbours' halos
-      kmir<<<ctas, PW * 32, psmem, st>>>(src, dst, pitch, nx, ny, wt, s, geo, *mir);
+      kmir<<<ctas, PW * 32, psmem, st>>>(src, dst, pitch, nx, ny, wt, s, geo, *mir, cnt);
     else
-      kern<<<ctas, PW * 32, psmem, st>>>(src, dst, pitch, nx, ny, wt, s, geo, none);
+      kern<<<ctas, PW * 32, psmem, st>>>(src, dst, pitch, nx, ny, wt, s, geo, none, cnt);
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
     src = dst;
@@ -512,11 +531,12 @@ int launch_pipe_kernel(const Plan& p, const Geometry& geo, const T* d_in, T* d_o
 
 template <typename T>
 int launch_pipe(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch,
-                int nx, int ny, const T w[5], int64_t steps, cudaStream_t st) {
+                int nx, int ny, const T w[5], int64_t steps, cudaStream_t st,
+                unsigned long long* cnt) {
   constexpr int K = sizeof(T) == 8 ? 4 : 8;
   Weights<T> wt{w[0], w[1], w[2], w[3], w[4]};
   const bool sym = weights_isotropic<T>(w);
-#define DTB_GO(S, D) return launch_pipe_kernel<T, K, S, D>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, st)
+#define DTB_GO(S, D) return launch_pipe_kernel<T, K, S, D>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, st, cnt)
   if (sym) {
     if (p.dyn()) DTB_GO(true, true);
     DTB_GO(true, false);

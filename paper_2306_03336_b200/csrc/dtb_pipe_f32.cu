@@ -2,4 +2,5 @@
 #include "dtb_pipe.cuh"
 
 template int dtb::launch_pipe<float>(const Plan&, const Geometry&, const float*, float*,
-                                     int64_t, int, int, const float*, int64_t, cudaStream_t);
+                                     int64_t, int, int, const float*, int64_t, cudaStream_t,
+                                      unsigned long long*);

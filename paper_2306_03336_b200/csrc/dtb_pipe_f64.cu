@@ -3,7 +3,8 @@
 #include "dtb_pipe.cuh"
 
 template int dtb::launch_pipe<double>(const Plan&, const Geometry&, const double*, double*,
-                                      int64_t, int, int, const double*, int64_t, cudaStream_t);
+                                      int64_t, int, int, const double*, int64_t, cudaStream_t,
+                                      unsigned long long*);
 
 // debug builds (-DDTB_PIPE_PROBE=1): per pipe stage {wait_in, wait_out, total}
 // SM cycles, summed over warps since the last call (fp64 kernels); resets

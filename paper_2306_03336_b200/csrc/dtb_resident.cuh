@@ -24,7 +24,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
 resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ xb0,
                 T* __restrict__ xb1, int* __restrict__ flags, int64_t pitch, int nx, int ny,
                 Weights<T> wt, int64_t total_steps, int h, int poison,
-                unsigned long long* __restrict__ trace, const __grid_constant__ Geometry geo) {
+                unsigned long long* __restrict__ trace, const __grid_constant__ Geometry geo,
+                unsigned long long* __restrict__ cnt) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* tile = reinterpret_cast<T*>(smem_raw);
   const int tx = blockIdx.x % geo.ntx, ty = blockIdx.x / geo.ntx;
@@ -37,6 +38,9 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
   g2s_rows<T, K>(tile, in, pitch, gx0, gy0, 0, Lh, 0, Lw);
   cp_async_wait_all();
   __syncthreads();
+  if (cnt && threadIdx.x == 0)  // domain cells of the load (the ghost ring is not counted)
+    atomicAdd(cnt + 0, (unsigned long long)(span_in(gy0, gy0 + Lh, 1, ny + 1) *
+                                            span_in(gx0, gx0 + Lw, 1, nx + 1)));
 
   // how deep each neighbour's load region reaches into my owned cells
   const int bl = tx > 0 ? max(0, geo.col[tx - 1].w - cx.x) : 0;
@@ -90,7 +94,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     pub.g = pub.g0 + (threadIdx.x & 31) * K;
     // 1. compute the epoch; each warp publishes its band right after its last sweep
     advance<T, K, SYM, DYN>(tile, Lw, Lh, steps, wt, poison != 0, hl, hr, ht, hb,
-                            (last || poison) ? nullptr : &pub);
+                            (last || poison) ? nullptr : &pub, cnt, ox1 - ox0);
     done += steps;
     DTB_MARK(t_comp)
     if (last) break;
@@ -102,6 +106,9 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
       s2g_rows<T, K>(tile, xb, pitch, gx0, gy0, b0, oy1, ox0, ox1);
       s2g_rows<T, K>(tile, xb, pitch, gx0, gy0, t1, b0, ox0, ox0 + bl);
       s2g_rows<T, K>(tile, xb, pitch, gx0, gy0, t1, b0, max(ox1 - br, ox0 + bl), ox1);
+      if (cnt && threadIdx.x == 0)
+        atomicAdd(cnt + 1, (unsigned long long)((t1 - oy0 + oy1 - b0) * (ox1 - ox0) +
+                                                (b0 - t1) * (bl + ox1 - max(ox1 - br, ox0 + bl))));
       __syncthreads();
       if (threadIdx.x == 0) st_release_gpu(flags + vcta, epoch);
     }
@@ -110,7 +117,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     unsigned long long t_poll = tc;
     refresh_by_direction<T, K>(tile, xb, pitch, gx0, gy0, flags, epoch * flag_per_epoch,
                                geo.ntx, geo.nty, tx, ty, ry0, oy0, oy1, ry1, rx0, ox0, ox1,
-                               rx1, tracing ? &t_poll : nullptr);
+                               rx1, tracing ? &t_poll : nullptr, cnt);
     if (tracing) {
       t_wait += t_poll - tc;  // warp 0: until its first neighbour flag arrived
       tc = t_poll;
@@ -124,12 +131,14 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
     tr[0] = t_comp; tr[1] = 0; tr[2] = t_wait; tr[3] = t_ref; tr[4] = epoch;
   }
   s2g_rows<T, K>(tile, out, pitch, gx0, gy0, oy0 - !ht, oy1 + !hb, ox0 - !hl, ox1 + !hr);
+  if (cnt && threadIdx.x == 0)  // owned cells (the ghost ring copy is not counted)
+    atomicAdd(cnt + 1, (unsigned long long)((oy1 - oy0) * (ox1 - ox0)));
 }
 
 template <typename T, int K, int NW, bool SYM, bool DYN>
 int launch_resident_kernel(const Plan& p, const Geometry& geo, const T* d_in, T* d_out,
                            int64_t pitch, int nx, int ny, const Weights<T>& wt, int64_t steps,
-                           bool poison, cudaStream_t st) {
+                           bool poison, cudaStream_t st, unsigned long long* cnt) {
   const bool tracing = (g_flags & DTB_FLAG_TRACE) != 0;
   const int threads = NW * 32;
   const int64_t tiles = p.ctas;
@@ -165,7 +174,7 @@ int launch_resident_kernel(const Plan& p, const Geometry& geo, const T* d_in, T*
   int pois = poison ? 1 : 0;
   void* args[] = {(void*)&d_in, (void*)&d_out, (void*)&xb0, (void*)&xb1, (void*)&flags,
                   (void*)&pitch, (void*)&nx, (void*)&ny, (void*)&wt, (void*)&steps,
-                  (void*)&h, (void*)&pois, (void*)&trace, (void*)&geo};
+                  (void*)&h, (void*)&pois, (void*)&trace, (void*)&geo, (void*)&cnt};
   CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(p.ctas), dim3(threads), args,
                                        (size_t)smem, st));
   g_launches += 1;
@@ -184,7 +193,7 @@ int launch_resident_kernel(const Plan& p, const Geometry& geo, const T* d_in, T*
 template <typename T>
 int launch_resident_impl(const Plan& p, const Geometry& geo, const T* d_in, T* d_out,
                          int64_t pitch, int nx, int ny, const T w[5], int64_t steps, bool poison,
-                         cudaStream_t st) {
+                         cudaStream_t st, unsigned long long* cnt) {
   constexpr int K = sizeof(T) == 8 ? 4 : 8, NW = 8;
   if (p.K != K || p.warps != NW)
     return fail(DTB_EINFEASIBLE, "no resident kernel for elem %d K %d warps %d", (int)sizeof(T),
@@ -192,7 +201,7 @@ int launch_resident_impl(const Plan& p, const Geometry& geo, const T* d_in, T* d
   Weights<T> wt{w[0], w[1], w[2], w[3], w[4]};
   const bool sym = weights_isotropic<T>(w);
 #define DTB_GO(S, D) \
-  return launch_resident_kernel<T, K, NW, S, D>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st)
+  return launch_resident_kernel<T, K, NW, S, D>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st, cnt)
   if (sym) {
     if (p.dyn()) DTB_GO(true, true);
     DTB_GO(true, false);
@@ -204,8 +213,9 @@ int launch_resident_impl(const Plan& p, const Geometry& geo, const T* d_in, T* d
 
 template <typename T>
 int launch_resident(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch,
-                    int nx, int ny, const T w[5], int64_t steps, bool poison, cudaStream_t st) {
-  return launch_resident_impl<T>(p, geo, d_in, d_out, pitch, nx, ny, w, steps, poison, st);
+                    int nx, int ny, const T w[5], int64_t steps, bool poison, cudaStream_t st,
+                    unsigned long long* cnt) {
+  return launch_resident_impl<T>(p, geo, d_in, d_out, pitch, nx, ny, w, steps, poison, st, cnt);
 }
 
 }  // namespace dtb

@@ -2,4 +2,4 @@
 #include "dtb_resident.cuh"
 template int dtb::launch_resident<double>(const Plan&, const Geometry&, const double*, double*,
                                           int64_t, int, int, const double*, int64_t, bool,
-                                          cudaStream_t);
+                                          cudaStream_t, unsigned long long*);

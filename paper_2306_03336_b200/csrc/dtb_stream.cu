@@ -18,7 +18,8 @@ template <typename T, int K, int NW, bool SYM, bool DYN>
 __global__ void __launch_bounds__(NW * 32, 1)
 stream_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int nx, int ny,
               Weights<T> wt, int steps, int poison, int nbuf, int buf_elems,
-              unsigned long long* __restrict__ trace, const __grid_constant__ Geometry geo) {
+              unsigned long long* __restrict__ trace, const __grid_constant__ Geometry geo,
+              unsigned long long* __restrict__ cnt) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* bufs[2] = {reinterpret_cast<T*>(smem_raw), reinterpret_cast<T*>(smem_raw) + buf_elems};
   const bool tracing = trace != nullptr && threadIdx.x == 0;
@@ -55,7 +56,12 @@ stream_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int
     const int4 cx = geo.col[tx], cy = geo.row[ty];
     const int Lw = cx.w - cx.z, Lh = cy.w - cy.z;
     advance<T, K, SYM, DYN>(tile, Lw, Lh, steps, wt, poison != 0, cx.z > -1, cx.w < nx + 1,
-                            cy.z > -1, cy.w < ny + 1);
+                            cy.z > -1, cy.w < ny + 1, nullptr, cnt);
+    if (cnt && threadIdx.x == 0) {  // the tile's load and owned store (domain cells)
+      atomicAdd(cnt + 0, (unsigned long long)(span_in(cy.z + 1, cy.w + 1, 1, ny + 1) *
+                                              span_in(cx.z + 1, cx.w + 1, 1, nx + 1)));
+      atomicAdd(cnt + 1, (unsigned long long)((cy.y - cy.x) * (cx.y - cx.x)));
+    }
     DTB_MARK(t_comp)
     // owned cells, plus the ghost ring where the tile touches the domain edge
     const int sx0 = cx.x - (cx.x == 0), sx1 = cx.y + (cx.y == nx);
@@ -116,7 +122,7 @@ __global__ void fill_random_kernel(T* out, int64_t pitch, int nx, int ny, uint64
 template <typename T, int K, int NW, bool SYM, bool DYN>
 int launch_stream_kernel(const Plan& p, const Geometry& geo, const T* d_in, T* d_out,
                          int64_t pitch, int nx, int ny, const Weights<T>& wt, int64_t steps,
-                         bool poison, cudaStream_t st) {
+                         bool poison, cudaStream_t st, unsigned long long* cnt) {
   const bool tracing = (g_flags & DTB_FLAG_TRACE) != 0;
   const int threads = NW * 32;
   const int smem = (int)p.smem_bytes;
@@ -148,7 +154,7 @@ int launch_stream_kernel(const Plan& p, const Geometry& geo, const T* d_in, T* d
     T* dst = ((passes - 1 - i) % 2 == 0) ? d_out : tmp;
     kern<<<p.ctas, threads, (size_t)smem * nbuf, st>>>(src, dst, pitch, nx, ny, wt, s,
                                                        poison ? 1 : 0, nbuf, buf_elems, strace,
-                                                       geo);
+                                                       geo, cnt);
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
     src = dst;
@@ -166,7 +172,8 @@ int launch_stream_kernel(const Plan& p, const Geometry& geo, const T* d_in, T* d
 
 template <typename T>
 int launch_stream(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch,
-                  int nx, int ny, const T w[5], int64_t steps, bool poison, cudaStream_t st) {
+                  int nx, int ny, const T w[5], int64_t steps, bool poison, cudaStream_t st,
+                  unsigned long long* cnt) {
   constexpr int K = sizeof(T) == 8 ? 4 : 8, NW = 8;
   if (p.K != K || p.warps != NW)
     return fail(DTB_EINFEASIBLE, "no streaming kernel for elem %d K %d warps %d",
@@ -174,7 +181,7 @@ int launch_stream(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, i
   Weights<T> wt{w[0], w[1], w[2], w[3], w[4]};
   const bool sym = weights_isotropic<T>(w);
 #define DTB_GO(S, D) \
-  return launch_stream_kernel<T, K, NW, S, D>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st)
+  return launch_stream_kernel<T, K, NW, S, D>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, poison, st, cnt)
   if (sym) {
     if (p.dyn()) DTB_GO(true, true);
     DTB_GO(true, false);
@@ -210,7 +217,7 @@ int launch_fill(T* d_out, int64_t pitch, int nx, int ny, uint64_t seed, double g
 
 #define DTB_INST(T)                                                                            \
   template int launch_stream<T>(const Plan&, const Geometry&, const T*, T*, int64_t, int, int, \
-                                const T*, int64_t, bool, cudaStream_t);                        \
+                                const T*, int64_t, bool, cudaStream_t, unsigned long long*);   \
   template int launch_naive<T>(const T*, T*, T*, int64_t, int, int, const T*, int64_t,         \
                                cudaStream_t);                                                  \
   template int launch_fill<T>(T*, int64_t, int, int, uint64_t, double, int64_t, int64_t,       \

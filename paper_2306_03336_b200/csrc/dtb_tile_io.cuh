@@ -19,6 +19,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
+// number of [a, b) that lie in [lo, hi) (counting domain cells of copies)
+__device__ __forceinline__ long long span_in(long long a, long long b, long long lo, long long hi) {
+  return max(0LL, min(b, hi) - max(a, lo));
+}
+
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -125,7 +130,8 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
                                                      const int* flags, int epoch, int ntx, int nty,
                                                      int tx, int ty, int ry0, int oy0, int oy1,
                                                      int ry1, int rx0, int ox0, int ox1, int rx1,
-                                                     unsigned long long* mark = nullptr) {
+                                                     unsigned long long* mark = nullptr,
+                                                     unsigned long long* cnt = nullptr) {
   typedef Tile<T, K> L;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -154,6 +160,11 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
       polled = nb;
     }
     warp_g2s_chunks<T, K>(sbase, g, pitch, gx0, gy0, r0, r1, c0, c1, vec, lane);
+    if (cnt && lane == 0) {  // refreshed halo cells: loads and exchanged cells
+      const unsigned long long n = (unsigned long long)(r1 - r0) * (unsigned long long)(c1 - c0);
+      atomicAdd(cnt + 0, n);
+      atomicAdd(cnt + 2, n);
+    }
   }
   cp_async_wait_all();
 }
@@ -163,7 +174,9 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
 // along halo sides (the trapezoid rim, planner.py:272-286) plus the unused
 // lane columns. A stale read anywhere then propagates NaN into the owned
 // cells and fails the bitwise comparison (the reference's poison mode,
-// engine.py:16-20,174-177).
+// engine.py:16-20,174-177). The domain's ghost ring is exempt: it is frozen
+// and never refreshed, so a NaN there would be a stale value that a correct
+// schedule keeps reading (where a halo side meets the domain edge).
 template <typename T, int K>
 __device__ void poison_rim(T* tile, int Lw, int Lh, int done, bool hl, bool hr, bool ht, bool hb) {
   typedef Tile<T, K> L;
@@ -175,7 +188,9 @@ __device__ void poison_rim(T* tile, int Lw, int Lh, int done, bool hl, bool hr, 
     p |= hr && c >= Lw - done;
     p |= ht && r < done;
     p |= hb && r >= Lh - done;
-    if (p) tile[L::at(r, c)] = nanv;
+    const bool ghost = c < Lw && ((!ht && r == 0) || (!hb && r == Lh - 1) ||
+                                  (!hl && c == 0) || (!hr && c == Lw - 1));
+    if (p && !ghost) tile[L::at(r, c)] = nanv;
   }
 }
 
@@ -184,13 +199,14 @@ __device__ void poison_rim(T* tile, int Lw, int Lh, int done, bool hl, bool hr, 
 template <typename T, int K, bool SYM, bool DYN>
 __device__ void advance(T* tile, int Lw, int Lh, int steps, const Weights<T>& wt, bool poison,
                         bool hl, bool hr, bool ht, bool hb,
-                        const Publisher<T, K>* pub = nullptr) {
+                        const Publisher<T, K>* pub = nullptr,
+                        unsigned long long* cnt = nullptr, int owned_w = 0) {
   if (!poison) {
-    advance_tile<T, K, SYM, DYN>(tile, Lw, Lh, steps, wt, pub);
+    advance_tile<T, K, SYM, DYN>(tile, Lw, Lh, steps, wt, pub, cnt, owned_w);
     return;
   }
   for (int s = 0; s < steps; ++s) {
-    advance_tile<T, K, SYM, DYN>(tile, Lw, Lh, 1, wt);
+    advance_tile<T, K, SYM, DYN>(tile, Lw, Lh, 1, wt, nullptr, cnt);
     poison_rim<T, K>(tile, Lw, Lh, s + 1, hl, hr, ht, hb);
     __syncthreads();
   }

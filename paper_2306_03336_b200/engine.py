@@ -13,6 +13,7 @@ a missing library or CUDA failure raises :class:`EngineError`.
 from __future__ import annotations
 
 import ctypes
+import dataclasses
 from dataclasses import dataclass
 
 import numpy as np
@@ -111,10 +112,11 @@ def _solve_host(data: np.ndarray, nx: int, ny: int, weights, steps: int, t_depth
     return out, rep
 
 
-def _report(rep: _native.DtbReport) -> TrafficReport:
+def _report(rep: _native.DtbReport, counted: bool = False) -> TrafficReport:
     return TrafficReport(rep.global_load_cells, rep.global_store_cells, rep.halo_exchanged_cells,
                          rep.redundant_compute_cells, rep.useful_compute_cells,
-                         rep.scratchpad_peak_bytes, rep.elem_bytes)
+                         rep.scratchpad_peak_bytes, rep.elem_bytes,
+                         source="b200 counted" if counted else "b200 model")
 
 
 def run_dtb(grid, weights, total_steps: int, plan=None, cfg: KernelConfig = KernelConfig(), *,
@@ -146,24 +148,32 @@ def run_dtb(grid, weights, total_steps: int, plan=None, cfg: KernelConfig = Kern
                            ilp, flags, dtype)
     result = Grid2D(grid.nx, grid.ny, out.astype(np.float64, copy=False))
     if plan is not None:
-        return result, model_dtb_traffic(plan, total_steps, valid)
+        # the reference plan's counters (the reconciliation contract), labelled;
+        # the traffic of the B200 schedule that actually ran rides along
+        model = model_dtb_traffic(plan, total_steps, valid)
+        return result, dataclasses.replace(model, source="reference-plan model",
+                                           b200=_report(rep))
     return result, _report(rep)
 
 
 def run_dtb_b200(grid, weights, total_steps: int, *, valid=None, poison: bool = False,
-                 dtype=np.float64, flags: int = 0, depth: int | None = None, n_gpus: int = 1
-                 ) -> tuple[Grid2D, TrafficReport]:
+                 dtype=np.float64, flags: int = 0, depth: int | None = None, n_gpus: int = 1,
+                 count: bool = False) -> tuple[Grid2D, TrafficReport]:
     """Like run_dtb without a reference plan, returning the B200 schedule's own
     traffic (dtb_report). ``flags`` takes _native.FLAG_FORCE_* for tests;
     ``depth`` pins the temporal halo depth; ``n_gpus`` > 1 splits the grid
-    into y-slabs over the visible GPUs inside the library (one process)."""
+    into y-slabs over the visible GPUs inside the library (one process);
+    ``count`` reports the traffic the kernels counted instead of the model."""
     _check_valid(grid.nx, grid.ny, valid)
     if depth is not None:
         flags |= _native.FLAG_FORCE_DEPTH
+    if count:
+        flags |= _native.FLAG_COUNT
     out, rep = _solve_host(grid.data, grid.nx, grid.ny, weights, total_steps,
                            depth if depth is not None else 1, valid, 1,
                            flags | (_native.FLAG_POISON if poison else 0), dtype, n_gpus)
-    return Grid2D(grid.nx, grid.ny, out.astype(np.float64, copy=False)), _report(rep)
+    return (Grid2D(grid.nx, grid.ny, out.astype(np.float64, copy=False)),
+            _report(rep, counted=count))
 
 
 def j2d5pt(grid, weights, steps: int, *, dtype=np.float64) -> Grid2D:

@@ -2,15 +2,20 @@
 
 ``run_dtb`` returns a :class:`TrafficReport`. When the caller passes a
 reference-style :class:`~.planner.TilingPlan`, the report is that plan's
-analytic model — exactly the counters the reference engine reconciles to
-(``report == model_dtb_traffic(plan, steps, valid)``, test_engine.py:41-50).
-The B200 schedule's own traffic is returned by ``run_dtb_b200`` as a
-:class:`TrafficReport` filled from the native plan (dtb_report).
+model — exactly the counters the reference engine reconciles to
+(``report == model_dtb_traffic(plan, steps, valid)``, test_engine.py:41-50),
+labelled ``source="reference-plan model"``; the B200 never runs that
+serial-tile schedule, so the traffic of what did run rides along as
+``report.b200``. ``run_dtb_b200`` returns the B200 schedule's report
+directly: ``source="b200 model"`` (the analytic model of the schedule,
+dtb_host.cu fill_report) or, with ``count=True``, ``source="b200 counted"``
+(the kernels' device counters at their copy and compute sites; the tests
+require both to agree exactly).
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 from .grid import Rect
 from .planner import DEFAULT_ELEM_BYTES, tile_active_region
@@ -29,6 +34,9 @@ class TrafficReport:
     useful_compute_cells: int
     scratchpad_peak_bytes: int
     elem_bytes: int = DEFAULT_ELEM_BYTES
+    # provenance; not part of the reference's counters (not compared)
+    source: str = field(default="model", compare=False)
+    b200: "TrafficReport | None" = field(default=None, compare=False, repr=False)
 
     @property
     def global_load_bytes(self) -> int:

@@ -338,6 +338,8 @@ class SlabSolver:
                     lib.dtb_stream_wait_event(sp, ctypes.c_void_p(ipc.peer[r][1][1 - cur]))
             out_idx = 1 - in_idx
             m = self._mirror(out_idx)
+            if done + s >= total_steps:  # the last epoch feeds no one
+                m.peer[0] = m.peer[1] = None
             rc = fn(ptrs[in_idx], ptrs[out_idx], g.nx, g.local_ny, pitch, w, s, ctypes.byref(m),
                     sp, ctypes.byref(rep))
             if rc != _native.DTB_OK:

@@ -152,14 +152,23 @@ def test_fp32_matches_fp32_oracle(nx, ny):
             assert same(out.data.astype(np.float32), want), (nx, ny, steps, flags)
 
 
-def test_poison_mode_does_not_leak():
-    g = rgrid(129, 93, 7, ghost=1.5)
+@pytest.mark.parametrize("nx,ny", [(129, 93), (300, 260), (700, 520)])
+def test_poison_mode_does_not_leak(nx, ny):
+    """NaN-poison debug mode (engine.py:16-20,174-177): every cell a correct
+    schedule may no longer read is NaN-ed after each step; any stale read
+    would surface as NaN in the result. Resident (forced), tile-streaming and
+    default plans, several depths, multi-epoch runs."""
+    g = rgrid(nx, ny, 7, ghost=1.5)
     want = jacobi_c(g.data, W02.astuple(), 16)
-    for flags in (0, STREAM):
+    for flags in (0, STREAM, _native.FLAG_FORCE_RESIDENT):
         for depth in (2, 4, 8):
-            out, _ = run_dtb_b200(g, W02, 16, poison=True, flags=flags, depth=depth)
+            try:
+                out, _ = run_dtb_b200(g, W02, 16, poison=True, flags=flags, depth=depth)
+            except Exception as e:  # a forced resident plan may not fit this shape
+                assert "fit" in str(e) or "feasible" in str(e), e
+                continue
+            assert not np.isnan(out.data).any(), (flags, depth)
             assert same(out.data, want), (flags, depth)
-            assert not np.isnan(out.data).any()
 
 
 def test_determinism_and_input_untouched():
