@@ -1,3 +1,4 @@
-set -x
-python tools/poison_probe.py 2>&1 | tail -12
-timeout 600 python -m pytest tests/test_gpu_traffic.py tests/test_gpu_parity.py -q -k "poison or traffic" 2>&1 | tail -4
+for lib in ab/lib_head.so paper_2306_03336_b200/libdtb_b200.so ab/lib_notma.so ab/lib_w12.so ab/lib_w12notma.so; do
+echo "== $lib"
+DTB_LIB=$lib python tools/sweep_bench.py 16384:16384:1000:f64:0:- 8192:8192:1000:f32:0:- 2>&1 | cut -c1-150
+done
