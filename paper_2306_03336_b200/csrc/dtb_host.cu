@@ -261,7 +261,7 @@ void fill_report(const Plan& p, int64_t nx, int64_t ny, int64_t steps, bool pois
         const int rx0 = hl ? 0 : 1, rx1 = hr ? Lw : Lw - 1, ry0 = ht ? 0 : 1, ry1 = hb ? Lh : Lh - 1;
         load += span(gy0, gy0 + Lh, 1, ny + 1) * span(gx0, gx0 + Lw, 1, nx + 1);
         store += (int64_t)(oy1 - oy0) * (ox1 - ox0);
-        // refresh_by_direction's regions (dtb_tile_io.cuh)
+        // refresh_flat's ring, by owning neighbour (dtb_tile_io.cuh)
         int64_t refresh = 0;
         const int reg[8][6] = {{0, -1, ry0, oy0, ox0, ox1}, {0, 1, oy1, ry1, ox0, ox1},
                                {-1, -1, ry0, oy0, rx0, ox0}, {1, -1, ry0, oy0, ox1, rx1},

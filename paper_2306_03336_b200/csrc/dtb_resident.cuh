@@ -27,6 +27,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
                 unsigned long long* __restrict__ trace, const __grid_constant__ Geometry geo,
                 unsigned long long* __restrict__ cnt) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  typedef Tile<T, K> L;
   T* tile = reinterpret_cast<T*>(smem_raw);
   const int tx = blockIdx.x % geo.ntx, ty = blockIdx.x / geo.ntx;
   const int vcta = blockIdx.x;
@@ -54,7 +55,7 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
 
   int64_t done = 0;
   int epoch = 0;
-  unsigned long long t_comp = 0, t_wait = 0, t_ref = 0, tc = 0;
+  unsigned long long t_comp = 0, t_wait = 0, t_ref = 0, t_copy = 0, tc = 0;
   const bool tracing = trace != nullptr && threadIdx.x == 0;
   if (tracing) tc = clock64();
 #define DTB_MARK(acc)                          \
@@ -112,15 +113,24 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
       __syncthreads();
       if (threadIdx.x == 0) st_release_gpu(flags + vcta, epoch);
     }
-    // 2+3. per direction: a warp waits for the neighbour owning its halo
-    // region and streams that region in (the 8 waits and loads overlap)
-    unsigned long long t_poll = tc;
-    refresh_by_direction<T, K>(tile, xb, pitch, gx0, gy0, flags, epoch * flag_per_epoch,
-                               geo.ntx, geo.nty, tx, ty, ry0, oy0, oy1, ry1, rx0, ox0, ox1,
-                               rx1, tracing ? &t_poll : nullptr, cnt);
+    // 2+3. wait for the neighbours' epoch flags, stream the halo ring in
+    unsigned long long t_poll[2] = {tc, tc};
+    // (measured per type: the balanced split wins on 256-column fp32 tiles,
+    // C3a +6 %; one warp per neighbour on 128-column fp64 tiles, C2 +2 %)
+    if constexpr (sizeof(T) == 4) {
+      refresh_flat<T, K>(tile, xb, pitch, gx0, gy0, flags, epoch * flag_per_epoch, geo.ntx,
+                         geo.nty, tx, ty, ry0, oy0, oy1, ry1, rx0, ox0, ox1, rx1,
+                         tracing ? t_poll : nullptr, cnt);
+    } else {
+      refresh_by_direction<T, K>(tile, xb, pitch, gx0, gy0, flags, epoch * flag_per_epoch,
+                                 geo.ntx, geo.nty, tx, ty, ry0, oy0, oy1, ry1, rx0, ox0, ox1,
+                                 rx1, tracing ? t_poll : nullptr, cnt);
+      t_poll[1] = t_poll[0];
+    }
     if (tracing) {
-      t_wait += t_poll - tc;  // warp 0: until its first neighbour flag arrived
-      tc = t_poll;
+      t_wait += t_poll[0] - tc;  // warp 0: until the neighbour flags arrived
+      t_copy += t_poll[1] - t_poll[0];
+      tc = t_poll[1];
     }
     __syncthreads();
     DTB_MARK(t_ref)
@@ -128,7 +138,8 @@ resident_kernel(const T* __restrict__ in, T* __restrict__ out, T* __restrict__ x
 #undef DTB_MARK
   if (tracing) {
     unsigned long long* tr = trace + 8 * vcta;
-    tr[0] = t_comp; tr[1] = 0; tr[2] = t_wait; tr[3] = t_ref; tr[4] = epoch;
+    tr[0] = t_comp; tr[1] = 0; tr[2] = t_wait; tr[3] = t_ref + t_copy; tr[4] = epoch;
+    tr[5] = t_copy;
   }
   s2g_rows<T, K>(tile, out, pitch, gx0, gy0, oy0 - !ht, oy1 + !hb, ox0 - !hl, ox1 + !hr);
   if (cnt && threadIdx.x == 0)  // owned cells (the ghost ring copy is not counted)

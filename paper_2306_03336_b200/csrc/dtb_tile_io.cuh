@@ -29,6 +29,11 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release_gpu(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -92,6 +97,101 @@ __device__ __forceinline__ void s2g_rows(const T* tile, T* __restrict__ g, int64
   }
 }
 
+// Resident halo refresh, flattened: the ring — the full-width rows above and
+// below the owned block, then the W / E columns beside it, row by row — in
+// 16-byte chunks, split into NW equal contiguous shares, one per warp, after
+// warp 0 has seen every neighbour's epoch flag (lanes 0..7 poll one each,
+// acquire; a CTA barrier passes it on). Used for fp32 tiles (dtb_resident.cuh):
+// the per-direction split (one warp per neighbour) leaves the W / E warps
+// with ~30x the corner warps' chunks there (C3a 8 % slower); per-warp waits
+// for only the neighbours of the warp's share measured 1.7 % slower than
+// this barrier. `mark` (tracing): [0] flags seen, [1] warp 0's copy landed.
+template <typename T, int K>
+__device__ __forceinline__ void refresh_flat(T* tile, const T* __restrict__ g, int64_t pitch,
+                                             int gx0, int gy0, const int* flags, int epoch,
+                                             int ntx, int nty, int tx, int ty, int ry0, int oy0,
+                                             int oy1, int ry1, int rx0, int ox0, int ox1, int rx1,
+                                             unsigned long long* mark = nullptr,
+                                             unsigned long long* cnt = nullptr) {
+  typedef Tile<T, K> L;
+  constexpr int E = L::EPC;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(tile);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // whole 16-byte chunks move as one cp.async when the global rows are chunk-aligned
+  const bool vec = ((gx0 % E) == 0) && ((pitch % E) == 0);
+  // rects as scalars (a dynamically indexed array would land in local
+  // memory, which the flag acquire's L1 invalidation evicts)
+  const int qr = rx0 / E, nqr = rx1 > rx0 ? (rx1 + E - 1) / E - qr : 0;
+  const int qw = rx0 / E, nqw = ox0 > rx0 ? (ox0 + E - 1) / E - qw : 0;
+  const int qe = ox1 / E, nqe = rx1 > ox1 ? (rx1 + E - 1) / E - qe : 0;
+  const int nt = max(0, oy0 - ry0) * nqr, nb = max(0, ry1 - oy1) * nqr;
+  const int nm = max(0, oy1 - oy0);
+  const int tot = nt + nb + nm * (nqw + nqe);
+  const int i0 = (int)((int64_t)tot * warp / nw), i1 = (int)((int64_t)tot * (warp + 1) / nw);
+  if (threadIdx.x < 8) {  // warp 0, one neighbour per lane: N S NW NE SW SE W E
+    const int dx = lane == 0 || lane == 1 ? 0 : (lane == 2 || lane == 4 || lane == 6 ? -1 : 1);
+    const int dy = lane == 6 || lane == 7 ? 0 : (lane == 0 || lane == 2 || lane == 3 ? -1 : 1);
+    const bool rows = dy < 0 ? ry0 < oy0 : dy > 0 ? oy1 < ry1 : oy0 < oy1;
+    const bool cols = dx < 0 ? rx0 < ox0 : dx > 0 ? ox1 < rx1 : ox0 < ox1;
+    const int nxt = tx + dx, nyt = ty + dy;
+    if (rows && cols && nxt >= 0 && nxt < ntx && nyt >= 0 && nyt < nty) {
+#ifndef DTB_NOPOLL  // timing-only builds: no wait for the neighbour (wrong results)
+      const int* f = flags + nyt * ntx + nxt;
+      if (ld_acquire_gpu(f) < epoch) {
+        // spin without the acquire's L1 invalidation, then acquire once
+        while (ld_relaxed_gpu(f) < epoch) __nanosleep(32);
+        (void)ld_acquire_gpu(f);
+      }
+#endif
+    }
+  }
+  __syncthreads();  // every neighbour published (acquire by warp 0, barrier for the rest)
+  if (mark) mark[0] = clock64();
+  const uint64_t mr = nqr ? (0xFFFFFFFFull + (uint64_t)nqr) / (uint64_t)nqr : 0;
+  const uint64_t mw = nqw + nqe ? (0xFFFFFFFFull + (uint64_t)(nqw + nqe)) / (uint64_t)(nqw + nqe) : 0;
+  for (int i = i0 + lane; i < i1; i += 32) {
+    int r, q, c0, c1;
+    if (i < nt + nb) {  // a full-width row above or below the owned block
+      const int j = i < nt ? i : i - nt;
+      const uint32_t rr = (uint32_t)(((uint64_t)(uint32_t)j * mr) >> 32);
+      r = (i < nt ? ry0 : oy1) + (int)rr;
+      q = qr + j - (int)rr * nqr;
+      c0 = rx0;
+      c1 = rx1;
+    } else {  // W then E chunks of one owned row
+      const int j = i - nt - nb, w = nqw + nqe;
+      const uint32_t rr = (uint32_t)(((uint64_t)(uint32_t)j * mw) >> 32);
+      const int jj = j - (int)rr * w;
+      r = oy0 + (int)rr;
+      const bool west = jj < nqw;
+      q = west ? qw + jj : qe + jj - nqw;
+      c0 = west ? rx0 : ox1;
+      c1 = west ? ox0 : rx1;
+    }
+    const int cb = q * E;
+    const uint32_t sa = sbase + (uint32_t)((r * L::ROW + L::swz(q) * E) * (int)sizeof(T));
+    const T* src = g + (int64_t)(gy0 + r) * pitch + gx0 + cb;
+#ifndef DTB_NOREFRESH  // timing-only builds: no halo copy (wrong results)
+    if (vec && cb >= c0 && cb + E <= c1) {
+      cp_async16(sa, src);
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (cb + e >= c0 && cb + e < c1) cp_async(sa + (uint32_t)(e * sizeof(T)), src + e);
+    }
+#endif
+  }
+  if (cnt && threadIdx.x == 0) {  // refreshed halo cells: loads and exchanged cells
+    const unsigned long long c =
+        (unsigned long long)max(0, oy0 - ry0 + ry1 - oy1) * (unsigned long long)(rx1 - rx0) +
+        (unsigned long long)max(0, oy1 - oy0) * (unsigned long long)(ox0 - rx0 + rx1 - ox1);
+    atomicAdd(cnt + 0, c);
+    atomicAdd(cnt + 2, c);
+  }
+  cp_async_wait_all();
+  if (mark) mark[1] = clock64();
+}
+
 // Copy tile rect [r0, r1) x [c0, c1) from global by 16-byte smem chunks,
 // flattened over (row, chunk) across the 32 lanes of one warp. Whole chunks
 // use a 16-byte cp.async when the global side is aligned (vec).
@@ -123,7 +223,8 @@ __device__ __forceinline__ void warp_g2s_chunks(uint32_t sbase, const T* __restr
 // 8 regions (N, S, the 4 corners, W, E), each owned by one neighbour; warp k
 // polls that neighbour's epoch flag (acquire) and streams its region in with
 // cp.async as soon as it is published, so the waits and loads of the eight
-// directions overlap. `mark` (tracing): when warp 0's first flag arrived.
+// directions overlap. `mark` (tracing): [0] when warp 0's first flag arrived.
+// Chosen for fp64 (dtb_resident.cuh): C2 2 % faster than refresh_flat.
 template <typename T, int K>
 __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restrict__ g,
                                                      int64_t pitch, int gx0, int gy0,
@@ -153,13 +254,19 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
     if (r1 <= r0 || c1 <= c0 || nxt < 0 || nxt >= ntx || nyt < 0 || nyt >= nty) continue;
     const int nb = nyt * ntx + nxt;
     if (nb != polled) {
-      if (lane == 0)
-        while (ld_acquire_gpu(flags + nb) < epoch) __nanosleep(32);
+#ifndef DTB_NOPOLL  // timing-only builds: no wait for the neighbour (wrong results)
+      if (lane == 0 && ld_acquire_gpu(flags + nb) < epoch) {
+        while (ld_relaxed_gpu(flags + nb) < epoch) __nanosleep(32);
+        (void)ld_acquire_gpu(flags + nb);
+      }
+#endif
       __syncwarp();
       if (mark && polled < 0) *mark = clock64();
       polled = nb;
     }
+#ifndef DTB_NOREFRESH  // timing-only builds: no halo copy (wrong results)
     warp_g2s_chunks<T, K>(sbase, g, pitch, gx0, gy0, r0, r1, c0, c1, vec, lane);
+#endif
     if (cnt && lane == 0) {  // refreshed halo cells: loads and exchanged cells
       const unsigned long long n = (unsigned long long)(r1 - r0) * (unsigned long long)(c1 - c0);
       atomicAdd(cnt + 0, n);
