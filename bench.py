@@ -73,11 +73,17 @@ def measured_peaks():
 
 def ncu_traffic(kernel, dtype):
     """DRAM bytes (read + write) per launch of the dominant kernel from the
-    committed ncu --set full capture (profiles/r01/ncu_summary.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01", "ncu_summary.json")) as fh:
-            summ = json.load(fh)
-    except (OSError, ValueError):
+    newest committed ncu --set full capture (profiles/r02, else r01
+    ncu_summary.json), or None."""
+    summ = None
+    for rnd in ("r02", "r01"):
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "ncu_summary.json")) as fh:
+                summ = json.load(fh)
+            break
+        except (OSError, ValueError):
+            continue
+    if summ is None:
         return None, None
     tag = "double" if dtype == "f64" else "float"
     for name, rec in summ.items():
