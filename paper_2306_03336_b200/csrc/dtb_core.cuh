@@ -539,13 +539,20 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
   const int rows = Lh - 2;
   if (rows <= 0 || Lw <= 2) return;
   auto publish = [&](bool act, int ya, int yb) {
+#ifndef DTB_NOPUBLISH  // timing-only builds: no halo stores (wrong results)
     if (act) {
       const int64_t n = pub->put_band(la, ya, yb, owned_w);
       if (cnt && lc.lane == 0 && n) atomicAdd(cnt + 1, (unsigned long long)n);
     }
+#endif
     __syncwarp();
+#ifdef DTB_NOFENCE  // timing-only builds: flag without the release fence (racy)
+    if (lc.lane == 0)
+      asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
+#else
     if (lc.lane == 0)
       asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
+#endif
   };
   int s = 0;
   if (steps >= 2 && rows >= 2) {

@@ -389,3 +389,56 @@ def test_fuzz_every_entry_point():
     r = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz.py"), "300", "11"],
                        cwd=root, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_device_buffers_of_other_dtypes_are_rejected():
+    import torch
+    from paper_2306_03336_b200 import j2d5pt_device
+    from paper_2306_03336_b200.prng import fill_random_device, fill_random_rows_device
+    a = torch.zeros((18, 32), dtype=torch.float16, device="cuda")
+    with pytest.raises(ValueError, match="dtype"):
+        j2d5pt_device(a, a.clone(), 16, 16, W02, 2)
+    with pytest.raises(ValueError, match="dtype"):
+        fill_random_device(a, 16, 16, 1)
+    with pytest.raises(ValueError, match="dtype"):
+        fill_random_rows_device(a, 16, 16, 1, 0)
+    with pytest.raises(ValueError, match="dtype"):
+        fill_random_rows_device(a.float(), 16, 16, 1, 0)  # the row fill is fp64 only
+
+
+def test_offset_view_with_valid_window_leaves_outside_columns_untouched():
+    """with valid=, the frozen cells are copied with a 2-D copy of
+    the view's nx+2 columns only; the columns of the allocation outside the
+    view keep their sentinels (and an offset view reads nothing past its end)."""
+    import torch
+    from paper_2306_03336_b200 import j2d5pt_device
+    nx, ny, steps = 129, 77, 10
+    v = Rect(13, 5, 100, 60)
+    gg = rgrid(nx, ny, 11, ghost=0.5)
+    sentinel = -12345.5
+    base_in = torch.full((ny + 2, 1 + 160), sentinel, dtype=torch.float64, device="cuda")
+    base_in[:, 1:nx + 3] = torch.from_numpy(gg.data).cuda()
+    base_out = torch.full_like(base_in, sentinel)
+    j2d5pt_device(base_in[:, 1:], base_out[:, 1:], nx, ny, MIXED, steps, valid=v)
+    out = base_out.cpu().numpy()
+    assert (out[:, 0] == sentinel).all() and (out[:, nx + 3:] == sentinel).all()
+    sub = grid_extract(gg, v)
+    want = jacobi_c(sub.data, MIXED.astuple(), steps)
+    got = out[:, 1:nx + 3][v.y0:v.y0 + v.height + 2, v.x0:v.x0 + v.width + 2]
+    assert same(got, want)
+    # cells outside the valid window are carried over unchanged
+    full = out[:, 1:nx + 3].copy()
+    mask = np.ones_like(full, dtype=bool)
+    mask[v.y0 + 1:v.y0 + v.height + 1, v.x0 + 1:v.x0 + v.width + 1] = False
+    assert np.array_equal(full[mask].view(np.uint64), gg.data[mask].view(np.uint64))
+
+
+def test_device_entry_rejects_buffers_on_two_devices():
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    from paper_2306_03336_b200 import j2d5pt_device
+    a = torch.zeros((18, 32), dtype=torch.float64, device="cuda:0")
+    b = torch.zeros((18, 32), dtype=torch.float64, device="cuda:1")
+    with pytest.raises(ValueError, match="cuda:1"):
+        j2d5pt_device(a, b, 16, 16, W02, 2)

@@ -102,3 +102,20 @@ def test_host_entry_n_gpus_with_valid_region():
     sub = grid_extract(g, v)
     want = jacobi_c(sub.data, w.astuple(), 40)
     assert np.array_equal(one.data[v.y0:v.y0 + v.height + 2, v.x0:v.x0 + v.width + 2], want)
+
+
+@pytest.mark.parametrize("flags_name", ["FLAG_SLAB_FUSED", "FLAG_SLAB_COPY"])
+def test_host_entry_slabs_across_real_devices(flags_name):
+    """Slabs on distinct GPUs: the fused mode's in-kernel stores go to a peer
+    device over NVLink (peer access enabled and checked by the library, copy
+    mode otherwise). Skipped on boxes with one GPU."""
+    import torch
+    from paper_2306_03336_b200 import _native, run_dtb_b200
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs two or more GPUs")
+    nx, ny, steps = 1100, 900, 40
+    g = grid_new(nx, ny, random_interior(nx, ny, 5))
+    out, _ = run_dtb_b200(g, W, steps, n_gpus=min(n, 4), flags=getattr(_native, flags_name))
+    want = jacobi_c(g.data, W.astuple(), steps)
+    assert np.array_equal(out.data.view(np.uint64), want.view(np.uint64))

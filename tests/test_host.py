@@ -201,3 +201,17 @@ def test_infeasible_plan_carries_min_required_bytes():
     # success clears it
     plan_b200(256, 256, 8, 100, 1)
     assert _native.lib().dtb_last_min_required_bytes() == 0
+
+
+def test_device_entry_rejects_other_dtypes_before_any_cuda_call():
+    """a 2-byte or integer buffer must raise, not run the f32 path
+    with a pitch read in the wrong element size (checked before the device)."""
+    import torch
+    from paper_2306_03336_b200 import j2d5pt_device
+    w = StencilWeights.diffusive(0.2)
+    for dt in (torch.float16, torch.bfloat16, torch.int32, torch.int64):
+        a = torch.zeros((10, 12), dtype=dt)
+        with pytest.raises(ValueError, match="dtype"):
+            j2d5pt_device(a, a.clone(), 8, 8, w, 2)
+    with pytest.raises(TypeError):
+        j2d5pt_device(np.zeros((10, 10)), np.zeros((10, 10)), 8, 8, w, 2)
