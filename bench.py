@@ -94,7 +94,13 @@ def ncu_traffic(kernel, dtype):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region.
+
+    The nvidia-smi process is started when the sampler is created (before the
+    warm-up: it takes a few hundred ms to deliver its first sample); `with
+    sampler:` marks the timed window, and the summary keeps the samples that
+    arrived inside it (or, for a window shorter than the 50 ms period, the
+    first one after it)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -102,27 +108,34 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines = []
-
-    def __enter__(self):
+        self.lines = []  # (arrival time, line)
+        self.t0 = self.t1 = None
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                ["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except OSError:
             self.proc = None
-        return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.monotonic(), line.strip()))
+
+    def __enter__(self):
+        self.t0 = time.monotonic()
+        return self
 
     def __exit__(self, *exc):
+        self.t1 = time.monotonic()
         if self.proc is not None:
+            # a window shorter than the sampling period: wait for one sample
+            deadline = self.t1 + 1.0
+            while (not any(ts >= self.t0 for ts, _ in self.lines)
+                   and time.monotonic() < deadline and self.proc.poll() is None):
+                time.sleep(0.02)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -132,7 +145,13 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0 = self.t0 if self.t0 is not None else 0.0
+        t1 = self.t1 if self.t1 is not None else float("inf")
+        inside = [ln for ts, ln in self.lines if t0 <= ts <= t1 + 0.05]
+        if not inside:
+            after = [ln for ts, ln in self.lines if ts >= t0]
+            inside = after[:1]
+        for ln in inside:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -350,6 +369,7 @@ def slab_series(args, world, rank, local, ny, steps, exchange="auto"):
         if world > 1:
             dist.barrier()
 
+    clk = ClockSampler(local)  # started before the warm-up (first sample latency)
     for _ in range(args.warmup):
         fresh()
         solver.run(steps)
@@ -358,7 +378,7 @@ def slab_series(args, world, rank, local, ny, steps, exchange="auto"):
     total_ms = 0.0
     launches[0] = 0
     solver.launches = 0
-    with ClockSampler(local) as clk:
+    with clk:
         for _ in range(args.steps):
             fresh()
             torch.cuda.synchronize()
@@ -507,6 +527,7 @@ def run_single(args, world, rank, local):
             import torch.distributed as dist
             dist.barrier()
 
+    clk = ClockSampler(local)  # started before the warm-up (first sample latency)
     for _ in range(args.warmup):
         j2d5pt_device(a, b, nx, ny, w, steps)
     torch.cuda.synchronize()
@@ -516,7 +537,7 @@ def run_single(args, world, rank, local):
     launches = 0
     torch.cuda.synchronize()
     barrier()
-    with ClockSampler(local) as clk:
+    with clk:
         # solves are queued back to back, each bracketed by its own events, so
         # the ~20 us host cost of a call overlaps the previous solve and the
         # flush (it is part of the e2e leg below); multi-rank runs keep a
