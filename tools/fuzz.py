@@ -26,6 +26,9 @@ for c in range(n_cases):
     dt = np.float32 if rng.random() < 0.35 else np.float64
     g = grid_new(nx, ny, random_interior(nx, ny, c + seed), ghost=float(rng.choice([0.0, 0.375, -2.0])))
     w = StencilWeights(*(float(x) for x in rng.uniform(-0.7, 0.7, 5)))
+    if rng.random() < 0.35:  # isotropic (w = e = s = n): the shared-product kernels
+        a = float(rng.uniform(-0.7, 0.7))
+        w = StencilWeights(a, a, a, float(rng.uniform(-0.7, 0.7)), a)
     valid = None
     if rng.random() < 0.4 and nx > 2 and ny > 2:
         x0, y0 = int(rng.integers(0, nx - 1)), int(rng.integers(0, ny - 1))
@@ -72,6 +75,9 @@ for c in range(20):
     dst_base = torch.zeros_like(base)
     steps = int(rng.integers(1, 30))
     w = StencilWeights(*(float(x) for x in rng.uniform(-0.7, 0.7, 5)))
+    if rng.random() < 0.35:  # isotropic (w = e = s = n): the shared-product kernels
+        a = float(rng.uniform(-0.7, 0.7))
+        w = StencilWeights(a, a, a, float(rng.uniform(-0.7, 0.7)), a)
     j2d5pt_device(base[:, off:], dst_base[:, off:], nx, ny, w, steps)
     npdt = np.float64 if dt == torch.float64 else np.float32
     want = jacobi_c(g.data, w.astuple(), steps, npdt)
