@@ -367,15 +367,13 @@ struct Publisher {
     }
   }
   // publish the part of band [ya, yb) the neighbours read; returns the cells
-  // stored (whole owned rows: own1... the owned width; sides: wl + wr per row)
+  // stored (whole owned rows: the owned width; sides: wl + wr per row)
   __device__ __forceinline__ int64_t put_band(const LaneAddr<T, K>& la, int ya, int yb,
                                               int owned_w) const {
     const int r0 = max(ya, own0), r1 = min(yb, own1);
     const int s0 = max(r0, top1), s1 = min(r1, bot0);
 #ifndef DTB_NOSIDEPUB  // timing-only builds: no side-column publish (wrong results)
-#ifndef DTB_NOSIDEPUB  // timing-only builds: no side-column publish (wrong results)
     if (s0 < s1) put_sides(la, s0, s1);
-#endif
 #endif
     put_rows(la, r0, min(r1, top1));
     put_rows(la, max(r0, bot0), r1);
