@@ -149,12 +149,17 @@ bool plan_resident(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInf
   bool found = false;
   const char* mt = getenv("DTB_MAX_TILES");  // experiments: cap the resident tile count
   const int max_tiles = mt ? atoi(mt) : 1 << 30;
+  const char* ya = getenv("DTB_YALIGN");  // experiments: load-height alignment (rows - 2)
+  const int yalign_env = ya ? atoi(ya) : 0;
   for (const Shape& sh : shapes_for(elem)) {
     const int K = sh.K, W = sh.warps;
     const int Lw_max = 32 * K;
     const int64_t row_bytes = (int64_t)Lw_max * elem;
     const int maxRows = (int)((dev.smem_optin - 1024) / row_bytes);
     if (maxRows < 3) continue;
+    // no load-height padding: the band sweeps take any row count (padding
+    // rows-2 to a multiple of 4 bands x 8 rows cost C2 6 % and C3a 11 %)
+    const int yalign = yalign_env > 0 ? yalign_env : 1;
     for (int h : depths_for(depth)) {
       const int hh = (int)std::min<int64_t>(h, std::max<int64_t>(steps, 1));
       const int ntx_min = (int)((nx + 2 + Lw_max - 1) / Lw_max);
@@ -166,8 +171,7 @@ bool plan_resident(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInf
         for (int nty = nty_max; nty >= nty_lo; --nty) {
           if (ntx * nty > max_tiles) continue;
           Split sy;
-          // (L - 2) a multiple of 4 rows per band: the static sweep fast path
-          if (!make_split((int)ny, nty, h, W <= 8 ? 4 * W : 4, maxRows, nty > 1 ? h : 1, sy, 2)) continue;
+          if (!make_split((int)ny, nty, h, yalign, maxRows, nty > 1 ? h : 1, sy, 2)) continue;
           // cost per epoch of hh steps: slowest CTA + exchange
           double cyc = tile_cycles(elem, K, W, sy.max_load, hh);
           if (steps > hh) {
@@ -225,7 +229,7 @@ bool plan_streaming(int64_t nx, int64_t ny, int elem, int64_t steps, const DevIn
               1, std::max<int64_t>((ny + 2 + maxRows - 1) / maxRows, (ny + per_y - 1) / per_y - 1));
           for (int nty = nty0; nty <= std::min<int64_t>(ny, nty0 + 8); ++nty) {
           Split sy;
-          if (!make_split((int)ny, nty, h, 4 * W, maxRows, 1, sy, 2)) continue;
+          if (!make_split((int)ny, nty, h, 1, maxRows, 1, sy, 2)) continue;
           const int64_t ntiles = (int64_t)ntx * nty;
           const int64_t slots = dev.sms;  // one CTA per SM
           const double waves = std::ceil((double)ntiles / slots);
