@@ -5,9 +5,11 @@
 // SM); the whole grid stays in shared memory for the whole solve. Every h
 // steps each warp publishes the owned cells of its band that the neighbours'
 // halos cover into an L2-resident exchange buffer and bumps its CTA's epoch
-// flag (release-add); each halo region is then refreshed by a warp that polls
-// only the neighbour owning it (acquire) and streams the region in with
-// 16-byte cp.async. This replaces the reference's serial-tile BSP loop
+// flag (release-add); the halo ring is then refreshed with 16-byte cp.async
+// — on fp64 tiles by one warp per neighbour direction that polls only that
+// neighbour (acquire, refresh_by_direction), on fp32 tiles split evenly over
+// the warps after warp 0 has seen every flag (refresh_flat; dtb_tile_io.cuh).
+// This replaces the reference's serial-tile BSP loop
 // (engine.py:265-290) and its modelled grid-level barrier
 // with point-to-point neighbour synchronisation.
 #pragma once
