@@ -21,10 +21,11 @@ import numpy as np
 from . import _native
 from .grid import Grid2D, Rect, as_weights_tuple
 from .metrics import TrafficReport, model_dtb_traffic
-from .planner import InfeasiblePlanError, partition_widths
+from .planner import InfeasiblePlanError, partition_widths, tile_active_region
 
-__all__ = ["EngineError", "KernelConfig", "run_dtb", "run_dtb_b200", "j2d5pt", "jacobi",
-           "j2d5pt_device", "last_launch_count"]
+__all__ = ["EngineError", "KernelConfig", "run_dtb", "run_dtb_b200", "run_dtb_trace", "j2d5pt",
+           "j2d5pt_trace", "jacobi", "j2d5pt_device", "last_launch_count", "TileTrace",
+           "TileBlockTrace"]
 
 
 class EngineError(RuntimeError):
@@ -174,6 +175,112 @@ def run_dtb_b200(grid, weights, total_steps: int, *, valid=None, poison: bool = 
                            flags | (_native.FLAG_POISON if poison else 0), dtype, n_gpus)
     return (Grid2D(grid.nx, grid.ny, out.astype(np.float64, copy=False)),
             _report(rep, counted=count))
+
+
+@dataclass
+class TileBlockTrace:
+    """One time block at the probed tile (engine.py:215-222): the load-region
+    image after the load, one image per superstep, the stored interior."""
+
+    load: np.ndarray
+    steps: list
+    store: np.ndarray
+
+
+@dataclass
+class TileTrace:
+    """engine.py:225-229."""
+
+    tile_index: int
+    load_region: Rect
+    blocks: list
+
+
+def _superstep_image(base: np.ndarray, load: Rect, states: list, s: int, tile, valid: Rect,
+                     poison: bool) -> np.ndarray:
+    """The probed tile's assembled front buffer after superstep ``s`` of the
+    reference's double-buffered schedule (engine.py:178-194): state ``s`` on
+    the active trapezoid; outside it the buffer still holds the state its
+    parity last received (s-2, s-4, ..., down to the loaded block start), or
+    NaN on the valid cells in poison mode. ``states[t]`` is the padded grid
+    after t steps of the block, computed on the B200."""
+    img = base.copy()
+    if poison:
+        pv = load.intersect(valid)
+        img[pv.y0 - load.y0:pv.y1 - load.y0, pv.x0 - load.x0:pv.x1 - load.x0] = np.nan
+        ts = (s,)
+    else:
+        ts = range(2 if s % 2 == 0 else 1, s + 1, 2)
+    for t in ts:
+        a = tile_active_region(tile, t, valid)
+        if a.is_empty:
+            continue
+        img[a.y0 - load.y0:a.y1 - load.y0, a.x0 - load.x0:a.x1 - load.x0] = \
+            states[t][a.y0 + 1:a.y1 + 1, a.x0 + 1:a.x1 + 1]
+    return img
+
+
+def run_dtb_trace(grid, weights, total_steps: int, plan, cfg: KernelConfig = KernelConfig(), *,
+                  probe: int, valid=None, threads: int | None = None,
+                  poison: bool = False) -> tuple[Grid2D, TrafficReport, TileTrace]:
+    """Like :func:`run_dtb` but record the probed tile's buffers
+    (engine.py:329-345): per time block the load-region image after the load,
+    one image per superstep and the stored interior slice.
+
+    The states come from the B200: the solve advances one step per call so
+    every intermediate grid exists, and the images are assembled from them
+    with the reference schedule's buffer semantics (state s on the active
+    trapezoid, the parity's older states on the rim). Debug path: one launch
+    and one host round trip per step. Raises IndexError for a bad probe.
+    """
+    del threads
+    _check_plan(grid, total_steps, plan, valid, 8)
+    _check_valid(grid.nx, grid.ny, valid)
+    if not 0 <= probe < len(plan.tiles):
+        raise IndexError(f"probe tile {probe} out of range (plan has {len(plan.tiles)} tiles)")
+    vrect = valid if valid is not None else Rect(0, 0, grid.nx, grid.ny)
+    tile = plan.tiles[probe]
+    load, it = tile.load_region, tile.interior
+    ilp = cfg.ilp if cfg is not None else 1
+    flags = _native.FLAG_POISON if poison else 0
+    cur = np.array(grid.data, dtype=np.float64, copy=True)
+    blocks = []
+    for _ in range(total_steps // plan.t_depth):
+        states = [cur]
+        for _s in range(plan.t_depth):
+            nxt, _rep = _solve_host(states[-1], grid.nx, grid.ny, weights, 1, 1, valid, ilp,
+                                    flags, np.float64)
+            states.append(nxt)
+        base = cur[load.y0 + 1:load.y1 + 1, load.x0 + 1:load.x1 + 1].copy()
+        steps = [_superstep_image(base, load, states, s, tile, vrect, poison)
+                 for s in range(1, plan.t_depth + 1)]
+        cur = states[-1]
+        blocks.append(TileBlockTrace(base, steps,
+                                     cur[it.y0 + 1:it.y1 + 1, it.x0 + 1:it.x1 + 1].copy()))
+    model = model_dtb_traffic(plan, total_steps, valid)
+    return (Grid2D(grid.nx, grid.ny, cur), dataclasses.replace(model, source="reference-plan model"),
+            TileTrace(probe, load, blocks))
+
+
+def j2d5pt_trace(grid, weights, steps: int, stride: int = 1, *, dtype=np.float64) -> list:
+    """The B200 twin of jacobi_reference_trace (oracle.py:37-59): copies of the
+    state at t = 0, stride, 2*stride, ... plus always the final step, each one
+    B200 solve of ``stride`` steps from the previous snapshot (a solve of a+b
+    steps equals a solve of a then b, bitwise)."""
+    if steps < 0:
+        raise ValueError(f"steps must be non-negative, got {steps}")
+    if stride < 1:
+        raise ValueError(f"stride must be at least 1, got {stride}")
+    cur = np.array(grid.data, dtype=np.float64, copy=True)
+    out = [Grid2D(grid.nx, grid.ny, cur.copy())]
+    t = 0
+    while t < steps:
+        n = min(stride - t % stride, steps - t)
+        nxt, _ = _solve_host(cur, grid.nx, grid.ny, weights, n, 1, None, 1, 0, dtype)
+        cur = nxt.astype(np.float64, copy=False)
+        t += n
+        out.append(Grid2D(grid.nx, grid.ny, cur.copy()))
+    return out
 
 
 def j2d5pt(grid, weights, steps: int, *, dtype=np.float64) -> Grid2D:
