@@ -39,7 +39,6 @@
 namespace dtb {
 
 constexpr int kPipeStages = 4;   // stage warps per pipeline (2 steps each): h = 8
-constexpr int kPipeWarps = 16;   // 4 pipelines per CTA, one per SM sub-partition
 
 #if DTB_PIPE_PROBE
 __device__ unsigned long long g_pipe_probe[8][3];
@@ -65,6 +64,12 @@ __device__ __forceinline__ void pipe_commit() { asm volatile("cp.async.commit_gr
 // the cells, so half the compute per row to hide a row's latency behind).
 template <typename T>
 struct PipeCfg {
+  // lane width and warps per CTA: a 1 KB row per warp-row, 16 warps = 4
+  // pipelines, one per SM sub-partition (fp64 K=8 x 8 warps, 2 KB rows, fewer
+  // shuffles and selects per cell, measured 11 % slower on C4: two warps per
+  // sub-partition leave the FP64 latency exposed)
+  static constexpr int kK = sizeof(T) == 8 ? 4 : 8;
+  static constexpr int kWarps = 16;
   static constexpr bool kDeep = sizeof(T) == 8;
   static constexpr int kRing0Rows = kDeep ? 16 : 12;  // stage 0's HBM prefetch ring
   static constexpr int kRingRows = 12;                // ring between stages
@@ -550,7 +555,7 @@ template <typename T, int K, bool SYM, bool DYN>
 int launch_pipe_kernel(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch,
                        int nx, int ny, const Weights<T>& wt, int64_t steps, cudaStream_t st,
                        unsigned long long* cnt) {
-  constexpr int S = kPipeStages, PW = kPipeWarps, P = PW / S;
+  constexpr int S = kPipeStages, PW = PipeCfg<T>::kWarps, P = PW / S;
   auto kern = pipe_kernel<T, K, PW, S, SYM, DYN, false>;
   auto kmir = pipe_kernel<T, K, PW, S, SYM, DYN, true>;
   const int pipe_bytes = (PipeCfg<T>::kRing0Rows + (S - 1) * PipeCfg<T>::kRingRows) *
@@ -598,7 +603,10 @@ template <typename T>
 int launch_pipe(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch,
                 int nx, int ny, const T w[5], int64_t steps, cudaStream_t st,
                 unsigned long long* cnt) {
-  constexpr int K = sizeof(T) == 8 ? 4 : 8;
+  constexpr int K = PipeCfg<T>::kK;
+  if (p.K != K || p.warps != PipeCfg<T>::kWarps)
+    return fail(DTB_EINFEASIBLE, "no pipe kernel for elem %d K %d warps %d", (int)sizeof(T), p.K,
+                p.warps);
   Weights<T> wt{w[0], w[1], w[2], w[3], w[4]};
   const bool sym = weights_isotropic<T>(w);
 #define DTB_GO(S, D) return launch_pipe_kernel<T, K, S, D>(p, geo, d_in, d_out, pitch, nx, ny, wt, steps, st, cnt)

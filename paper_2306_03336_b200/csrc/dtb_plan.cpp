@@ -80,7 +80,10 @@ namespace {
 struct Shape { int K; int warps; };
 
 // dtb_pipe.cuh kPipeWarps / kPipeStages / PipeCfg
-constexpr int kPlanPipeWarps = 16, kPlanPipeStages = 4;
+constexpr int kPlanPipeStages = 4;
+// lane width and warps per CTA of the pipe kernel per element size (PipeCfg)
+constexpr int plan_pipe_K(int elem) { return elem == 8 ? 4 : 8; }
+constexpr int plan_pipe_warps(int) { return 16; }
 
 // kernel shapes compiled into libdtb_b200.so (dtb_resident.cuh / dtb_stream.cu):
 // 32 B of row state per lane (fp64 K=4, fp32 K=8: one 1 KB smem row per
@@ -276,7 +279,8 @@ bool plan_streaming(int64_t nx, int64_t ny, int elem, int64_t steps, const DevIn
 // a few long segments so that there are about two pipelines' worth of
 // segments per SM.
 bool plan_pipe(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& dev, Plan& best) {
-  const int K = elem == 8 ? 4 : 8, W = kPlanPipeWarps, S = kPlanPipeStages, P = W / S, h = 2 * S;
+  const int K = plan_pipe_K(elem), W = plan_pipe_warps(elem), S = kPlanPipeStages, P = W / S,
+            h = 2 * S;
   const int Lw_max = 32 * K;
   const int per = Lw_max - 2 * h;
   Split sx;
@@ -284,9 +288,22 @@ bool plan_pipe(int64_t nx, int64_t ny, int elem, int64_t steps, const DevInfo& d
   for (; ntx <= nx; ++ntx)
     if (make_split((int)nx, ntx, h, K, Lw_max, 1, sx, 0, 16 / elem)) break;
   if (ntx > nx) return false;
+  // segments per strip: every pipeline marches ceil(tiles / pipelines) tiles
+  // (waves) of ~ny/nseg + 2h rows plus a pipeline fill; pick the count that
+  // minimises that (one wave when the strips alone fill the device, several
+  // shorter waves when they would leave SMs idle)
   const int64_t want = (int64_t)dev.sms * P;
-  int nseg = (int)std::max<int64_t>(1, want / ntx);  // at most one tile per pipeline
-  nseg = (int)std::min<int64_t>(nseg, std::max<int64_t>(1, ny / (2 * h)));
+  const int64_t seg_max = std::max<int64_t>(1, ny / (2 * h));
+  int nseg = 0;
+  double best_rows = 0;
+  for (int64_t n = 1; n <= std::min<int64_t>(seg_max, 4 * want); ++n) {
+    const int64_t waves = (ntx * n + want - 1) / want;
+    const double rows = (double)waves * ((double)(ny + n - 1) / n + 2 * h + 4 * S);
+    if (nseg == 0 || rows < best_rows * 0.999) {
+      nseg = (int)n;
+      best_rows = rows;
+    }
+  }
   Split sy;
   for (; nseg >= 1; --nseg)
     if (make_split((int)ny, nseg, h, 1, 1 << 30, nseg > 1 ? h : 1, sy)) break;
