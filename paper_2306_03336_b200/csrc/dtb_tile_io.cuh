@@ -135,14 +135,12 @@ __device__ __forceinline__ void refresh_flat(T* tile, const T* __restrict__ g, i
     const bool cols = dx < 0 ? rx0 < ox0 : dx > 0 ? ox1 < rx1 : ox0 < ox1;
     const int nxt = tx + dx, nyt = ty + dy;
     if (rows && cols && nxt >= 0 && nxt < ntx && nyt >= 0 && nyt < nty) {
-#ifndef DTB_NOPOLL  // timing-only builds: no wait for the neighbour (wrong results)
       const int* f = flags + nyt * ntx + nxt;
       if (ld_acquire_gpu(f) < epoch) {
         // spin without the acquire's L1 invalidation, then acquire once
         while (ld_relaxed_gpu(f) < epoch) __nanosleep(32);
         (void)ld_acquire_gpu(f);
       }
-#endif
     }
   }
   __syncthreads();  // every neighbour published (acquire by warp 0, barrier for the rest)
@@ -171,7 +169,6 @@ __device__ __forceinline__ void refresh_flat(T* tile, const T* __restrict__ g, i
     const int cb = q * E;
     const uint32_t sa = sbase + (uint32_t)((r * L::ROW + L::swz(q) * E) * (int)sizeof(T));
     const T* src = g + (int64_t)(gy0 + r) * pitch + gx0 + cb;
-#ifndef DTB_NOREFRESH  // timing-only builds: no halo copy (wrong results)
     if (vec && cb >= c0 && cb + E <= c1) {
       cp_async16(sa, src);
     } else {
@@ -179,7 +176,6 @@ __device__ __forceinline__ void refresh_flat(T* tile, const T* __restrict__ g, i
       for (int e = 0; e < E; ++e)
         if (cb + e >= c0 && cb + e < c1) cp_async(sa + (uint32_t)(e * sizeof(T)), src + e);
     }
-#endif
   }
   if (cnt && threadIdx.x == 0) {  // refreshed halo cells: loads and exchanged cells
     const unsigned long long c =
@@ -254,19 +250,15 @@ __device__ __forceinline__ void refresh_by_direction(T* tile, const T* __restric
     if (r1 <= r0 || c1 <= c0 || nxt < 0 || nxt >= ntx || nyt < 0 || nyt >= nty) continue;
     const int nb = nyt * ntx + nxt;
     if (nb != polled) {
-#ifndef DTB_NOPOLL  // timing-only builds: no wait for the neighbour (wrong results)
       if (lane == 0 && ld_acquire_gpu(flags + nb) < epoch) {
         while (ld_relaxed_gpu(flags + nb) < epoch) __nanosleep(32);
         (void)ld_acquire_gpu(flags + nb);
       }
-#endif
       __syncwarp();
       if (mark && polled < 0) *mark = clock64();
       polled = nb;
     }
-#ifndef DTB_NOREFRESH  // timing-only builds: no halo copy (wrong results)
     warp_g2s_chunks<T, K>(sbase, g, pitch, gx0, gy0, r0, r1, c0, c1, vec, lane);
-#endif
     if (cnt && lane == 0) {  // refreshed halo cells: loads and exchanged cells
       const unsigned long long n = (unsigned long long)(r1 - r0) * (unsigned long long)(c1 - c0);
       atomicAdd(cnt + 0, n);

@@ -1,8 +1,8 @@
 #!/bin/bash
 # Build an A/B variant of libdtb_b200.so into ab/lib_<name>.so with extra
-# -D defines (e.g. tools/build_variants.sh probe DTB_PIPE_PROBE=1). Timing-only
-# switches (DTB_NOPOLL, DTB_NOREFRESH, DTB_NOPUBLISH, DTB_NOFENCE, DTB_NOSIDEPUB)
-# build a library that solves only with DTB_TIMING_ONLY_OK=1 set.
+# -D defines (e.g. tools/build_variants.sh probe DTB_PIPE_PROBE=1). The
+# timing-only exchange switches (DTB_NOPOLL, ...) live in
+# tools/experiments/timing_only_exchange.patch.
 set -e
 cd "$(dirname "$0")/.."
 mkdir -p ab
