@@ -719,6 +719,216 @@ int solve_host_slabs(const T* in, T* out, int64_t nx, int64_t ny, int64_t pitch,
   return DTB_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Host-buffer solves of streaming plans: the passes run as a temporal
+// wavefront over row blocks (launch_pipe_wave) so that the host copies
+// overlap compute. The input is copied block by block on a copy stream and
+// each diagonal waits only for the blocks its first-pass tasks read; each
+// final row block is copied back as soon as its last-pass task's diagonal is
+// done. Without this the PCIe copies of C4 (2 x 2.15 GB) sit serially around
+// 125 passes.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct WaveStreams {  // per device, created once (the C ABI is externally synchronous)
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> ev;
+};
+WaveStreams g_wave[64];
+
+template <typename T>
+struct WaveCopies {
+  const T* in;
+  T* out;
+  T* d_in;
+  T* d_out;
+  int64_t pitch, dpitch, nx, ny;
+  int J;
+  std::vector<int64_t> r0, r1;  // padded rows of row block j (ghost rows at the ends)
+  cudaStream_t st, h2d, d2h;
+  cudaEvent_t* ev;              // [0, J): input block landed; [J, 2J): output block final
+  int waited = -1;
+};
+
+template <typename T>
+int wave_in_ready(void* c, int j) {  // the next launch reads input row blocks <= j
+  WaveCopies<T>& w = *static_cast<WaveCopies<T>*>(c);
+  if (j > w.waited) {
+    CUDA_TRY(cudaStreamWaitEvent(w.st, w.ev[j], 0));
+    w.waited = j;
+  }
+  return DTB_OK;
+}
+
+template <typename T>
+int wave_out_done(void* c, int j) {  // output row block j is final once `st` gets here
+  WaveCopies<T>& w = *static_cast<WaveCopies<T>*>(c);
+  cudaEvent_t e = w.ev[w.J + j];
+  CUDA_TRY(cudaEventRecord(e, w.st));
+  CUDA_TRY(cudaStreamWaitEvent(w.d2h, e, 0));
+  const size_t row = (size_t)(w.nx + 2) * sizeof(T);
+  CUDA_TRY(cudaMemcpy2DAsync(w.out + w.r0[j] * w.pitch, w.pitch * sizeof(T),
+                             w.d_out + w.r0[j] * w.dpitch, w.dpitch * sizeof(T), row,
+                             w.r1[j] - w.r0[j], cudaMemcpyDeviceToHost, w.d2h));
+  return DTB_OK;
+}
+
+// rows per wavefront row block (DTB_WAVE_ROWS, 0 = off): more blocks overlap
+// more of the copies, each block adds 2h rows of pass halo
+int64_t wave_rows() {
+  const char* e = getenv("DTB_WAVE_ROWS");
+  return e ? atoll(e) : 192;
+}
+
+// passes per wavefront phase: ~3/4 of the passes the host copy of the grid
+// takes (PCIe ~50 GB/s against ~1.35 / 1.9 Tcells/s per fp64 / fp32 pass).
+// B200, C4 e2e (profiles/r02/ab_wave*.log): 192-row blocks with 20 passes
+// 1142 GCells/s, 26 -> 1131, 32 -> 1117, 10 -> 1069; 128 / 256 rows 1128 /
+// 1118; no wavefront 979.
+int64_t wave_passes(int64_t nx, int64_t ny, int elem, int64_t passes) {
+  if (const char* e = getenv("DTB_WAVE_PASSES")) return std::max<int64_t>(1, atoll(e));
+  const double copy_s = (double)(nx + 2) * (ny + 2) * elem / 50e9;
+  const double pass_s = (double)nx * ny * 8 / (elem == 8 ? 1.35e12 : 1.9e12);
+  return std::min<int64_t>(passes, (int64_t)std::ceil(0.75 * copy_s / pass_s));
+}
+
+}  // namespace
+
+// returns DTB_OK after a wavefront solve, -1 when the plan is not a
+// multi-pass streaming plan (the caller solves the plain way)
+template <typename T>
+int solve_host_wave(const T* in, T* out, int64_t nx, int64_t ny, int64_t pitch, const T w[5],
+                    int64_t total_steps, unsigned flags, dtb_report* rep) {
+  const int64_t rows = wave_rows();
+  if (rows <= 0 || g_halo_mirror ||
+      (flags & (DTB_FLAG_POISON | DTB_FLAG_TRACE | DTB_FLAG_FORCE_STREAM | DTB_FLAG_FORCE_NAIVE |
+                DTB_FLAG_FORCE_RESIDENT | DTB_FLAG_FORCE_DEPTH)))
+    return -1;
+  DevInfo dev;
+  if (int rc = query_dev(dev)) return rc;
+  Plan p;
+  char err[512];
+  int64_t min_bytes = 0;
+  if (!make_plan(nx, ny, (int)sizeof(T), total_steps, dev, force_mode(flags), 0, p, err,
+                 sizeof err, &min_bytes))
+    return plan_fail(err, min_bytes);
+  const int64_t passes = (total_steps + p.h - 1) / p.h;
+  if (p.mode != 3 || passes < 2) return -1;
+  // a diagonal carries about J / 2 row-block tasks of ntx strips each; unless
+  // that fills the device's pipelines twice over (narrow grids, e.g. C3b's 35
+  // strips) the wavefront costs more than the copies it hides
+  const int64_t pipes = (int64_t)dev.sms * (p.warps / 4);
+  const int J = (int)std::min<int64_t>(2 * kMaxWaveTasks - 2, std::max<int64_t>(2, ny / rows));
+  if (!getenv("DTB_WAVE_ROWS") && (int64_t)(J / 2) * p.sx.n < 2 * pipes) return -1;
+  Split sy;
+  int nj = J;
+  for (; nj >= 2; --nj)
+    if (make_split((int)ny, nj, p.h, 1, 1 << 30, p.h, sy)) break;
+  if (nj < 2) return -1;
+  Plan pw = p;  // the wavefront phases' row blocks
+  pw.sy = sy;
+  Geometry geo, gw;
+  if (int rc = fill_geometry(p, geo)) return rc;
+  if (int rc = fill_geometry(pw, gw)) return rc;
+  const int64_t m = wave_passes(nx, ny, (int)sizeof(T), passes);
+  int device;
+  CUDA_TRY(cudaGetDevice(&device));
+  if (device < 0 || device >= 64) return -1;
+  WaveStreams& ws = g_wave[device];
+  if (!ws.h2d) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&ws.h2d, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&ws.d2h, cudaStreamNonBlocking));
+  }
+  while ((int)ws.ev.size() < 2 * nj) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ws.ev.push_back(e);
+  }
+  const int64_t dpitch = (nx + 2 + 31) / 32 * 32;
+  const size_t bytes = (size_t)(ny + 2) * dpitch * sizeof(T);
+  void* io = nullptr;
+  if (int rc = arena_get(kArenaIo, device, 2 * bytes, &io)) return rc;
+  WaveCopies<T> c;
+  c.in = in;
+  c.out = out;
+  c.d_in = reinterpret_cast<T*>(io);
+  c.d_out = reinterpret_cast<T*>(reinterpret_cast<char*>(io) + bytes);
+  c.pitch = pitch;
+  c.dpitch = dpitch;
+  c.nx = nx;
+  c.ny = ny;
+  c.J = nj;
+  c.st = 0;
+  c.h2d = ws.h2d;
+  c.d2h = ws.d2h;
+  c.ev = ws.ev.data();
+  for (int j = 0; j < nj; ++j) {
+    c.r0.push_back(j == 0 ? 0 : sy.o0[j] + 1);
+    c.r1.push_back(j == nj - 1 ? ny + 2 : sy.o1[j] + 1);
+  }
+  g_launches = 0;
+  g_flags = flags;
+  g_trace.clear();
+  // the copy stream starts after earlier work on the solve stream (arena reuse)
+  CUDA_TRY(cudaEventRecord(ws.ev[0], c.st));
+  CUDA_TRY(cudaStreamWaitEvent(c.h2d, ws.ev[0], 0));
+  CUDA_TRY(cudaStreamWaitEvent(c.d2h, ws.ev[0], 0));
+  const size_t row = (size_t)(nx + 2) * sizeof(T);
+  for (int j = 0; j < nj; ++j) {
+    CUDA_TRY(cudaMemcpy2DAsync(c.d_in + c.r0[j] * dpitch, dpitch * sizeof(T), in + c.r0[j] * pitch,
+                               pitch * sizeof(T), row, c.r1[j] - c.r0[j], cudaMemcpyHostToDevice,
+                               c.h2d));
+    CUDA_TRY(cudaEventRecord(ws.ev[j], c.h2d));
+  }
+  unsigned long long* cnt = nullptr;
+  if (flags & DTB_FLAG_COUNT) {
+    void* cp = nullptr;
+    if (int rc = arena_get(kArenaCounters, device, 8 * sizeof(unsigned long long), &cp)) return rc;
+    cnt = static_cast<unsigned long long*>(cp);
+    CUDA_TRY(cudaMemsetAsync(cnt, 0, 8 * sizeof(unsigned long long), c.st));
+  }
+  PipeWaveHooks hooks{&c, wave_in_ready<T>, wave_out_done<T>};
+  int rc = launch_pipe_wave<T>(p, geo, gw, c.d_in, c.d_out, dpitch, (int)nx, (int)ny, w,
+                               total_steps, m, c.st, cnt, hooks);
+  // drain both copy streams even after an error (no copy may outlive the call)
+  const cudaError_t e1 = cudaStreamSynchronize(c.h2d), e2 = cudaStreamSynchronize(c.d2h),
+                    e3 = cudaStreamSynchronize(c.st);
+  if (rc) return rc;
+  CUDA_TRY(e1);
+  CUDA_TRY(e2);
+  CUDA_TRY(e3);
+  if (rep) {  // the model of what ran: wavefront phases on pw's row blocks, the middle on p's
+    const int64_t mA = std::max<int64_t>(1, std::min(m, passes));
+    const int64_t mC = std::min<int64_t>(m, passes - mA);
+    const int64_t sA = std::min<int64_t>(total_steps, mA * p.h);
+    const int64_t sC = mC ? total_steps - (passes - mC) * p.h : 0;
+    const int64_t sB = total_steps - sA - sC;
+    memset(rep, 0, sizeof *rep);
+    const struct { const Plan* plan; int64_t steps; } parts[3] = {{&pw, sA}, {&p, sB}, {&pw, sC}};
+    for (const auto& part : parts) {
+      if (part.steps <= 0) continue;
+      dtb_report r;
+      fill_report<T>(*part.plan, nx, ny, part.steps, false, nullptr, &r);
+      rep->global_load_cells += r.global_load_cells;
+      rep->global_store_cells += r.global_store_cells;
+      rep->halo_exchanged_cells += r.halo_exchanged_cells;
+      rep->redundant_compute_cells += r.redundant_compute_cells;
+      rep->useful_compute_cells += r.useful_compute_cells;
+      rep->scratchpad_peak_bytes = r.scratchpad_peak_bytes;
+      rep->elem_bytes = r.elem_bytes;
+    }
+  }
+  if (cnt && rep) {
+    unsigned long long h[8];
+    CUDA_TRY(cudaMemcpy(h, cnt, sizeof h, cudaMemcpyDeviceToHost));
+    rep->global_load_cells = (int64_t)h[0];
+    rep->global_store_cells = (int64_t)h[1];
+    rep->halo_exchanged_cells = (int64_t)h[2];
+    rep->redundant_compute_cells = (int64_t)h[3] - nx * ny * total_steps;
+  }
+  return DTB_OK;
+}
+
 template <typename T>
 int solve_host(const T* in, T* out, int64_t nx, int64_t ny, int64_t pitch, const T w[5],
                int64_t total_steps, int64_t t_depth, const dtb_rect* valid, int ilp, int n_gpus,
@@ -742,6 +952,10 @@ int solve_host(const T* in, T* out, int64_t nx, int64_t ny, int64_t pitch, const
                                  total_steps, flags, n_gpus, rep);
     }
     return solve_host_slabs<T>(in, out, nx, ny, pitch, w, total_steps, flags, n_gpus, rep);
+  }
+  if (!valid || (valid->x0 == 0 && valid->y0 == 0 && valid->width == nx && valid->height == ny)) {
+    rc = solve_host_wave<T>(in, out, nx, ny, pitch, w, total_steps, flags, rep);
+    if (rc >= 0) return rc;
   }
   int device;
   CUDA_TRY(cudaGetDevice(&device));

@@ -17,6 +17,7 @@ namespace dtb {
 template <typename T> struct Weights;
 
 constexpr int kMaxTiles = 512;  // per dimension
+constexpr int kMaxWaveTasks = 72;  // (pass, row block) tasks per wavefront diagonal
 
 // Tile geometry as kernel parameters (<= 32 KB param space on sm_70+ / CUDA 12.1+).
 // col[i] = (owned x0, owned x1, load x0, load x1) in interior coordinates.
@@ -87,6 +88,19 @@ template <typename T>
 int launch_pipe(const Plan& p, const Geometry& geo, const T* d_in, T* d_out, int64_t pitch,
                 int nx, int ny, const T w[5], int64_t steps, cudaStream_t st,
                 unsigned long long* cnt);
+// launch_pipe_wave (dtb_pipe.cuh): in_ready(j) before a launch that reads
+// input row blocks <= j, out_done(j) after the launch that finishes output
+// row block j (host copies go between); a nonzero return aborts
+struct PipeWaveHooks {
+  void* ctx;
+  int (*in_ready)(void* ctx, int j);
+  int (*out_done)(void* ctx, int j);
+};
+template <typename T>
+int launch_pipe_wave(const Plan& p, const Geometry& geo, const Geometry& gw, const T* d_in,
+                     T* d_out, int64_t pitch, int nx, int ny, const T w[5], int64_t steps,
+                     int64_t m, cudaStream_t st, unsigned long long* cnt,
+                     const PipeWaveHooks& hooks);
 template <typename T>
 int launch_naive(const T* d_in, T* d_out, T* d_tmp, int64_t pitch, int nx, int ny, const T w[5],
                  int64_t steps, cudaStream_t st);

@@ -470,6 +470,18 @@ struct PipeSmem {
   int prod[S], cons[S];
 };
 
+// One wavefront diagonal (launch_pipe_wave): n (pass, row block) tasks, each
+// all column strips of row block ty advanced by `steps` steps from src to dst
+// (the pass's parity buffers). Empty (n == 0): the plain pass over every tile.
+template <typename T>
+struct PipeWave {
+  int n;
+  int ty[kMaxWaveTasks];
+  int steps[kMaxWaveTasks];
+  const T* src[kMaxWaveTasks];
+  T* dst[kMaxWaveTasks];
+};
+
 // One pass of up to 2S fused steps: NW/S pipelines of S warps per CTA, each
 // pipeline marching column-strip segments. Warp w runs stage w / P of
 // pipeline w % P, so each SM sub-partition (warp % 4) hosts one whole
@@ -478,7 +490,8 @@ template <typename T, int K, int NW, int S, bool SYM, bool DYN, bool MIR>
 __global__ void __launch_bounds__(NW * 32, 1)
 pipe_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int nx, int ny,
             Weights<T> wt, int steps, const __grid_constant__ Geometry geo,
-            const __grid_constant__ HaloMirror<T> mir, unsigned long long* __restrict__ cnt) {
+            const __grid_constant__ HaloMirror<T> mir, unsigned long long* __restrict__ cnt,
+            const __grid_constant__ PipeWave<T> wave) {
   constexpr int P = NW / S;
   typedef Tile<T, K> L;
   constexpr int RB = L::ROW * (int)sizeof(T);
@@ -497,14 +510,24 @@ pipe_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int n
   // ring s (s >= 1) follows ring0
   const uint32_t ring_in = s == 0 ? pbase : pbase + (uint32_t)(kRing0Rows + (s - 1) * kRingRows) * RB;
   const uint32_t ring_out = pbase + (uint32_t)(kRing0Rows + s * kRingRows) * RB;
-  const int levels = max(0, min(2, steps - 2 * s));
   LaneCtx lc;
   lc.lane = threadIdx.x & 31;
   lc.first = lc.lane == 0;
-  const int ntiles = geo.ntx * geo.nty;
+  const int ntiles = geo.ntx * (wave.n ? wave.n : geo.nty);
   int seq = 0;
   for (int t = blockIdx.x * P + p; t < ntiles; t += gridDim.x * P) {
-    const int tx = t % geo.ntx, ty = t / geo.ntx;
+    int tx = t % geo.ntx, ty = t / geo.ntx;
+    const T* tsrc = src;
+    T* tdst = dst;
+    int tsteps = steps;
+    if (wave.n) {  // wavefront task ty of this diagonal: its row block and buffers
+      const int k = ty;
+      ty = wave.ty[k];
+      tsrc = wave.src[k];
+      tdst = wave.dst[k];
+      tsteps = wave.steps[k];
+    }
+    const int levels = max(0, min(2, tsteps - 2 * s));
     const int4 cx = geo.col[tx], cy = geo.row[ty];
     PipeTile pt;
     pt.Lw = cx.w - cx.z;
@@ -524,7 +547,7 @@ pipe_kernel(const T* __restrict__ src, T* __restrict__ dst, int64_t pitch, int n
     pt.vec = ((pt.gx0 % L::EPC) == 0) && ((pitch % L::EPC) == 0);
     lc.last = lc.lane == (pt.Lw - 1) / K;
     lc.last_e = (pt.Lw - 1) % K;
-    pipe_stage<T, K, SYM, DYN, MIR>(pt, s, S, levels, seq, src, dst, pitch, ring_in, ring_out,
+    pipe_stage<T, K, SYM, DYN, MIR>(pt, s, S, levels, seq, tsrc, tdst, pitch, ring_in, ring_out,
                                     ctl[p].prod, ctl[p].cons, wt, lc, &mir);
     if (cnt && lc.lane == 0) {  // counted traffic (domain cells only)
       const long long dc = span_in(pt.gx0, pt.gx0 + pt.Lw, 1, nx + 1);
@@ -579,6 +602,8 @@ int launch_pipe_kernel(const Plan& p, const Geometry& geo, const T* d_in, T* d_o
   const HaloMirror<T>* mir = static_cast<const HaloMirror<T>*>(g_halo_mirror);
   HaloMirror<T> none;
   memset(&none, 0, sizeof none);
+  PipeWave<T> nowave;
+  nowave.n = 0;
   if (mir) {
     if (int rc = prepare_kernel((const void*)kmir, device, psmem, PW * 32, nullptr)) return rc;
   }
@@ -588,15 +613,128 @@ int launch_pipe_kernel(const Plan& p, const Geometry& geo, const T* d_in, T* d_o
     const int s = (int)std::min<int64_t>(2 * S, steps - done);
     T* dst = ((passes - 1 - i) % 2 == 0) ? d_out : tmp;
     if (mir && i + 1 == passes)  // the epoch's result: also feed the neighbours' halos
-      kmir<<<ctas, PW * 32, psmem, st>>>(src, dst, pitch, nx, ny, wt, s, geo, *mir, cnt);
+      kmir<<<ctas, PW * 32, psmem, st>>>(src, dst, pitch, nx, ny, wt, s, geo, *mir, cnt, nowave);
     else
-      kern<<<ctas, PW * 32, psmem, st>>>(src, dst, pitch, nx, ny, wt, s, geo, none, cnt);
+      kern<<<ctas, PW * 32, psmem, st>>>(src, dst, pitch, nx, ny, wt, s, geo, none, cnt, nowave);
     g_launches += 1;
     CUDA_TRY(cudaGetLastError());
     src = dst;
     done += s;
   }
   return DTB_OK;
+}
+
+// Passes as temporal wavefronts where host copies can overlap them. Task
+// (k, j) = pass k (1-based, steps 8(k-1)+1 .. 8k) on row block j of the wave
+// geometry (gw.row). It reads row blocks j-1..j+1 of pass k-1's output (the
+// 8-row halos stay inside the neighbours) and overwrites block j of the buffer
+// pass k-2 wrote, which only passes k-1 on blocks j-1..j+1 read. So the tasks
+// of one diagonal d = 2k + j depend only on earlier diagonals and not on each
+// other: one launch per diagonal, in order on `st`.
+//   phase A: passes 1..mA as a wavefront; a diagonal waits only for the input
+//            row blocks its first-pass tasks read (hooks.in_ready),
+//   phase B: the middle passes as plain full-grid passes (p / geo: long
+//            segments, no wave overheads),
+//   phase C: the last mC passes as a wavefront; each final row block is
+//            handed to hooks.out_done as soon as its diagonal is launched.
+// The wavefront phases cost extra row-block halos and shorter segments, so
+// they only cover about as many passes as the host copy they hide (m).
+template <typename T, int K, bool SYM, bool DYN>
+int launch_pipe_wave_kernel(const Plan& p, const Geometry& geo, const Geometry& gw,
+                            const T* d_in, T* d_out, int64_t pitch, int nx, int ny,
+                            const Weights<T>& wt, int64_t steps, int64_t m, cudaStream_t st,
+                            unsigned long long* cnt, const PipeWaveHooks& hooks) {
+  constexpr int S = kPipeStages, PW = PipeCfg<T>::kWarps, P = PW / S, h = 2 * S;
+  auto kern = pipe_kernel<T, K, PW, S, SYM, DYN, false>;
+  const int pipe_bytes = (PipeCfg<T>::kRing0Rows + (S - 1) * PipeCfg<T>::kRingRows) *
+                         Tile<T, K>::ROW * (int)sizeof(T);
+  const int psmem = P * pipe_bytes + (int)sizeof(PipeSmem<S>) * P;
+  int device;
+  CUDA_TRY(cudaGetDevice(&device));
+  if (int rc = prepare_kernel((const void*)kern, device, psmem, PW * 32, nullptr)) return rc;
+  const int J = gw.nty;
+  const int64_t passes = (steps + h - 1) / h;
+  if (J < 1 || J > 2 * kMaxWaveTasks - 2 || passes < 2 || gw.ntx != geo.ntx)
+    return fail(DTB_EINVAL, "wavefront of %d row blocks x %lld passes", J, (long long)passes);
+  T* tmp = nullptr;
+  {
+    void* scratch = nullptr;
+    const size_t grid_bytes = (size_t)(ny + 2) * pitch * sizeof(T);
+    if (int rc = arena_get(kArenaScratch, device, grid_bytes, &scratch)) return rc;
+    tmp = reinterpret_cast<T*>(scratch);
+  }
+  DevInfo di;
+  if (int rc = query_dev(di)) return rc;
+  HaloMirror<T> none;
+  memset(&none, 0, sizeof none);
+  PipeWave<T> wave;
+  auto dst_of = [&](int64_t k) { return ((passes - k) % 2 == 0) ? d_out : tmp; };  // k 1-based
+  auto src_of = [&](int64_t k) -> const T* { return k == 1 ? d_in : dst_of(k - 1); };
+  auto steps_of = [&](int64_t k) { return (int)std::min<int64_t>(h, steps - (k - 1) * h); };
+  // passes [k0, k1] as one wavefront
+  auto wavefront = [&](int64_t k0, int64_t k1) -> int {
+    const int64_t n = k1 - k0 + 1;
+    for (int64_t d = 2; d <= 2 * n + J - 1; ++d) {
+      wave.n = 0;
+      int need = -1;  // input row blocks the first-pass tasks read
+      for (int64_t q = std::min<int64_t>(n, d / 2); q >= 1 && d - 2 * q < J; --q) {
+        const int j = (int)(d - 2 * q), k = (int)(k0 + q - 1);
+        wave.ty[wave.n] = j;
+        wave.steps[wave.n] = steps_of(k);
+        wave.src[wave.n] = src_of(k);
+        wave.dst[wave.n] = dst_of(k);
+        ++wave.n;
+        if (k == 1) need = std::min(j + 1, J - 1);
+      }
+      if (need >= 0 && hooks.in_ready)
+        if (int rc = hooks.in_ready(hooks.ctx, need)) return rc;
+      const int ctas = (int)std::min<int64_t>(di.sms, ((int64_t)wave.n * gw.ntx + P - 1) / P);
+      kern<<<ctas, PW * 32, psmem, st>>>(d_in, d_out, pitch, nx, ny, wt, h, gw, none, cnt, wave);
+      g_launches += 1;
+      CUDA_TRY(cudaGetLastError());
+      // the last pass's task on block d - 2n is in this launch: that block is final
+      if (k1 == passes && d - 2 * n >= 0 && hooks.out_done)
+        if (int rc = hooks.out_done(hooks.ctx, (int)(d - 2 * n))) return rc;
+    }
+    return DTB_OK;
+  };
+  const int64_t mA = std::max<int64_t>(1, std::min(m, passes));
+  const int64_t mC = std::min<int64_t>(m, passes - mA);
+  if (int rc = wavefront(1, mA)) return rc;
+  wave.n = 0;
+  const int ctas = (int)std::min<int64_t>(di.sms, ((int64_t)geo.ntx * geo.nty + P - 1) / P);
+  for (int64_t k = mA + 1; k <= passes - mC; ++k) {
+    kern<<<ctas, PW * 32, psmem, st>>>(src_of(k), dst_of(k), pitch, nx, ny, wt, steps_of(k), geo,
+                                       none, cnt, wave);
+    g_launches += 1;
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (mC > 0)
+    if (int rc = wavefront(passes - mC + 1, passes)) return rc;
+  return DTB_OK;
+}
+
+template <typename T>
+int launch_pipe_wave(const Plan& p, const Geometry& geo, const Geometry& gw, const T* d_in,
+                     T* d_out, int64_t pitch, int nx, int ny, const T w[5], int64_t steps,
+                     int64_t m, cudaStream_t st, unsigned long long* cnt,
+                     const PipeWaveHooks& hooks) {
+  constexpr int K = PipeCfg<T>::kK;
+  if (p.K != K || p.warps != PipeCfg<T>::kWarps || p.mode != 3)
+    return fail(DTB_EINFEASIBLE, "no pipe kernel for elem %d K %d warps %d", (int)sizeof(T), p.K,
+                p.warps);
+  Weights<T> wt{w[0], w[1], w[2], w[3], w[4]};
+  const bool sym = weights_isotropic<T>(w);
+#define DTB_GO(S, D)                                                                          \
+  return launch_pipe_wave_kernel<T, K, S, D>(p, geo, gw, d_in, d_out, pitch, nx, ny, wt, steps, \
+                                              m, st, cnt, hooks)
+  if (sym) {
+    if (p.dyn()) DTB_GO(true, true);
+    DTB_GO(true, false);
+  }
+  if (p.dyn()) DTB_GO(false, true);
+  DTB_GO(false, false);
+#undef DTB_GO
 }
 
 template <typename T>

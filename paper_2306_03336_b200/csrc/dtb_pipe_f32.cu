@@ -3,4 +3,8 @@
 
 template int dtb::launch_pipe<float>(const Plan&, const Geometry&, const float*, float*,
                                      int64_t, int, int, const float*, int64_t, cudaStream_t,
-                                      unsigned long long*);
+                                     unsigned long long*);
+template int dtb::launch_pipe_wave<float>(const Plan&, const Geometry&, const Geometry&,
+                                        const float*, float*, int64_t, int, int, const float*,
+                                        int64_t, int64_t, cudaStream_t, unsigned long long*,
+                                        const PipeWaveHooks&);

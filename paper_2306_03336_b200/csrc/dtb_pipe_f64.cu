@@ -5,6 +5,10 @@
 template int dtb::launch_pipe<double>(const Plan&, const Geometry&, const double*, double*,
                                       int64_t, int, int, const double*, int64_t, cudaStream_t,
                                       unsigned long long*);
+template int dtb::launch_pipe_wave<double>(const Plan&, const Geometry&, const Geometry&,
+                                        const double*, double*, int64_t, int, int, const double*,
+                                        int64_t, int64_t, cudaStream_t, unsigned long long*,
+                                        const PipeWaveHooks&);
 
 // debug builds (-DDTB_PIPE_PROBE=1): per pipe stage {wait_in, wait_out, total}
 // SM cycles, summed over warps since the last call (fp64 kernels); resets
