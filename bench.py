@@ -541,7 +541,12 @@ def run_single(args, world, rank, local):
         # solves are queued back to back, each bracketed by its own events, so
         # the ~20 us host cost of a call overlaps the previous solve and the
         # flush (it is part of the e2e leg below); multi-rank runs keep a
-        # barrier per solve
+        # barrier per solve. A one-rank run first parks the stream on a ~5 ms
+        # device sleep (outside every event pair) so that the host enqueues
+        # the iterations ahead of the device: short solves (C1, ~0.1 ms)
+        # would otherwise time the host's ~45 us call latency as device idle
+        if world == 1:
+            torch.cuda._sleep(10_000_000)
         for i in range(args.steps):
             flush.fill_(i)  # evict the grid from L2 between timed iterations
             if world > 1:
