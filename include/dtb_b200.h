@@ -104,7 +104,12 @@ typedef struct dtb_plan_info {
  * slabs share a device when fewer are visible), exchanging 16-row halos by
  * device-to-device copies or in-kernel peer stores (NVLink P2P) — bitwise
  * equal to n_gpus = 1, with or without a valid region. The call stays
- * blocking. */
+ * blocking. Multi-pass streaming plans on one GPU overlap the host copies
+ * with compute: the input streams in by row blocks while the first passes run
+ * as a wavefront over the blocks that arrived, and the result streams out by
+ * row blocks as the last passes finish them (same bits; DTB_WAVE_ROWS=0 in
+ * the environment turns it off). In, out: pinned host memory lets the copies
+ * overlap; pageable memory works too. */
 int dtb_j2d5pt_f64(const double* in, double* out, int64_t nx, int64_t ny, int64_t pitch,
                    const double w[5], int64_t total_steps, int64_t t_depth,
                    const dtb_rect* valid, int ilp, int n_gpus, unsigned flags,
