@@ -53,7 +53,7 @@ __device__ __forceinline__ void pipe_cp_async(uint32_t dst, const double* src) {
 __device__ __forceinline__ void pipe_cp_async(uint32_t dst, const float* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
 }
-// 16-byte global stores of a lane's K-element row chunk, predicated (no
+// 16-byte global stores of a lane's 4-element fp64 row chunk, predicated (no
 // branch): the last stage's owned-row store in the steady loop. No "memory"
 // clobber: nothing in the kernel reads the destination, and the clobber would
 // pin the next rows' shared loads behind the store.
@@ -62,13 +62,6 @@ __device__ __forceinline__ void st_row_pred(bool p, double* g, const double (&v)
                " @q st.global.v2.f64 [%1], {%2, %3};\n"
                " @q st.global.v2.f64 [%1+16], {%4, %5}; }"
                ::"r"((unsigned)p), "l"(g), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3]));
-}
-__device__ __forceinline__ void st_row_pred(bool p, float* g, const float (&v)[8]) {
-  asm volatile("{ .reg .pred q; setp.ne.u32 q, %0, 0;\n"
-               " @q st.global.v4.f32 [%1], {%2, %3, %4, %5};\n"
-               " @q st.global.v4.f32 [%1+16], {%6, %7, %8, %9}; }"
-               ::"r"((unsigned)p), "l"(g), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]),
-                 "f"(v[5]), "f"(v[6]), "f"(v[7]));
 }
 
 template <int N>
